@@ -1,0 +1,346 @@
+"""Benchmark: edges/sec generated for BASELINE config 2 (n=1e7, k=32,
+gamma=2.5, T=0, seed 2) on N B200s, with the roofline of the range-query
+kernel and the reference algorithm's CPU time beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full generation (Philox sampling, band index build, count
+pass, scan, write pass, row ordering) of the whole graph; with N ranks each
+rank emits the rows of its angular sector, so the N ranks together produce
+the whole graph once per step (strong scaling over a fixed graph).
+Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    0: dict(n=10_000, avg_degree=6.0, gamma=3.0, seed=0),
+    1: dict(n=1_000_000, avg_degree=10.0, gamma=3.0, seed=1),
+    2: dict(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2),
+    3: dict(n=100_000_000, avg_degree=16.0, gamma=3.0, seed=3),
+}
+METRIC = "edges/sec generated (n=1e7,k=32,gamma=2.5)"
+UNIT = "edges/s"
+
+# algorithmic bytes of the range query:
+#   every point record is read once: phi, p_x, p_y, c_x, c_y, rad^2 (6 x f64),
+#   r, (1-r)(1+r) (2 x f32), id (i32)                       -> 60 B / vertex
+#   count pass writes a degree per vertex                     ->  4 B / vertex
+#   write pass reads a row offset per vertex and writes the CSR -> 8 B / vertex + 4 B / entry
+POINT_RECORD_B = 60
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--vertex-order", default="sample", choices=("sample", "angular"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=20_000,
+                    help="query vertices per CPU-baseline step (bounded sample)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, val in zip(names, r[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_reference_step(params, model, consts, n_queries, nthreads):
+    """The reference algorithm (oracle's polar-quadtree restatement, hrgen
+    quadtree.py) on the host: sample all points, build the tree over all of
+    them, answer a bounded sample of the vertex queries; returns the
+    extrapolated whole-graph edges/s and the pieces."""
+    from oracle import oracle as O
+    n = model.n
+    t0 = time.perf_counter()
+    u1, u2 = O.philox_uniforms(n, params["seed"])
+    phi, rn, rp = O.sample_from_uniforms(u1, u2, consts["two_over_alpha"],
+                                         consts["sinh_half_alpha_r"], consts["r_cap"],
+                                         consts["rp_cap"])
+    t_sample = time.perf_counter() - t0
+    nq = min(n, n_queries)
+    # a contiguous id range is a uniform sample of positions (ids are i.i.d.)
+    _, m_part, tm = O.edges_quadtree(phi, rp, consts["cosh_r_minus_1"], model.alpha,
+                                     consts["max_r"], 512, O.TRIG_LIBM, nthreads, 0, nq,
+                                     want_pairs=False)
+    frac = nq / n
+    # m_part counts edges (v, w>v) found from the sampled v; the expected
+    # share of all m found from a uniform fraction f of query vertices is f
+    m_est = m_part / frac
+    t_est = t_sample + tm.t_build_s + tm.t_query_s / frac
+    return m_est / t_est, dict(t_sample_s=t_sample, t_build_s=tm.t_build_s,
+                               t_query_sample_s=tm.t_query_s, queries=nq, m_est=m_est)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_1501_03545_b200 as P
+    params = CONFIGS[args.config]
+    gp = P.GeneratorParams(**params)
+    model = gp.resolve()
+    consts = P.model_constants(model.R, model.alpha)
+    nthreads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_step(params, model, consts, args.cpu_queries, nthreads)
+    vals, info = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, info = cpu_reference_step(params, model, consts, args.cpu_queries, nthreads)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = sorted(vals)[len(vals) // 2]
+    sample = (f"hrgen polar-quadtree algorithm (oracle/hrg_oracle.c restatement, libm trig): "
+              f"sample all {model.n} points + build the full tree + {info['queries']} vertex "
+              f"queries per step, whole-graph time extrapolated linearly in queries")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(params, model, args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": sample, **{k: v for k, v in info.items()}},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def config_block(params, model, args, world):
+    return {
+        "workload": f"config{args.config}: n={params['n']}, k={params['avg_degree']}, "
+                    f"gamma={params['gamma']} (alpha={model.alpha}), T=0, seed {params['seed']}",
+        "n": params["n"], "avg_degree": params["avg_degree"], "gamma": params["gamma"],
+        "alpha": model.alpha, "R": model.R, "seed": params["seed"],
+        "vertex_order": args.vertex_order,
+        "l2": "no flush: per-step working set (point records + CSR) >> 126 MB L2",
+        "parallelism": f"angular sectors x {world}" if world > 1 else "single GPU",
+    }
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1501_03545_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    params = CONFIGS[args.config]
+    gp = P.GeneratorParams(**params, vertex_order=args.vertex_order)
+    model = gp.resolve()
+    order = P.generator.VERTEX_ORDERS[args.vertex_order]
+    shard = P.Shard(rank, world) if world > 1 else None
+    eng = P.get_engine(local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        eng.generate(model, params["seed"], order, shard)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    qc, qw, launches, cand, nnz = [], [], 0, 0, 0
+    for _ in range(args.steps):
+        st = eng.generate(model, params["seed"], order, shard)
+        qc.append(st.t_query_count_ms)
+        qw.append(st.t_query_write_ms)
+        launches += st.kernel_launches
+        cand, nnz = st.candidates, st.nnz
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / max(args.steps, 1)
+
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([nnz, cand], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    nnz_all, cand_all = float(tot[0].item()), float(tot[1].item())
+    m_total = nnz_all / 2.0
+    value = m_total / (ms_max / 1e3)
+
+    # ---- e2e: the public API, results land in host memory (pinned int64 CSR)
+    e2e = None
+    if not args.no_e2e:
+        k2 = max(1, min(args.steps, 3))
+        P.generate_with_stats(gp, device=local, shard=shard)  # warm the pinned pool
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            g, s = P.generate_with_stats(gp, device=local, shard=shard)
+        torch.cuda.synchronize()
+        dt = torch.tensor([(time.perf_counter() - t0) / k2], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        d2h = (model.n + 1) * 8 + int(g.indices.size) * 8
+        e2e = {"value": m_total / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(dt.item()),
+               "api": "paper_1501_03545_b200.generate_with_stats -> host Graph (int64 CSR, "
+                      "pinned); inputs are the 5 scalar parameters"}
+        del g
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (write pass of the range query)
+    peak, peak_kind = load_peaks()
+    n_q = model.n / world
+    tw = sorted(qw)[len(qw) // 2]
+    tc = sorted(qc)[len(qc) // 2]
+    bytes_write = model.n * POINT_RECORD_B + n_q * 8 + (nnz_all / world) * 4
+    bytes_count = model.n * POINT_RECORD_B + n_q * 4
+    achieved = bytes_write / (tw / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "query_write_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as fh:
+                tj = json.load(fh)
+            if tj.get("config") == args.config and tj.get("n_gpus", 1) == world:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "k_query<write> (range query, CSR emission)",
+                "algorithmic_bytes_per_launch": bytes_write, "launch_ms": tw,
+                "count_pass": {"launch_ms": tc, "algorithmic_bytes": bytes_count,
+                               "achieved_gbs": bytes_count / (tc / 1e3) / 1e9},
+                "fp64": {"pair_tests": cand_all / world, "flop_per_test": 6,
+                         "tflops_count_pass": cand_all / world * 6 / (tc / 1e3) / 1e12}}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            consts = P.model_constants(model.R, model.alpha)
+            nthreads = os.cpu_count() or 1
+            v, info = cpu_reference_step(params, model, consts, args.cpu_queries, nthreads)
+            cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
+                   "sample": f"oracle polar quadtree (hrgen algorithm): all {model.n} points "
+                             f"sampled + full tree + {info['queries']} vertex queries, "
+                             f"whole-graph time extrapolated", **info}
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(params, model, args, world),
+        "m": m_total, "candidates": cand_all,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,176 @@
+"""ctypes wrapper over oracle/libhrg_oracle.so.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference leg, never by the product package.
+Each wrapper names the reference function (hrgen file:line) it restates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhrg_oracle.so")
+
+TRIG_LIBM = 0
+TRIG_CR = 1
+
+_lib = None
+
+_d = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class QtTiming(ctypes.Structure):
+    _fields_ = [("t_build_s", ctypes.c_double), ("t_query_s", ctypes.c_double),
+                ("t_csr_s", ctypes.c_double)]
+
+
+def build():
+    subprocess.check_call(["sh", os.path.join(HERE, "build.sh")])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        _u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.orc_philox_raw.argtypes = [_u32p, _u32p, _u32p]
+        L.orc_philox_uniforms.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _d, _d]
+        L.orc_sample_from_uniforms.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                               _d, _d, _d]
+        L.orc_circle_params.argtypes = [ctypes.c_int64, _d, ctypes.c_double, _d, _d]
+        L.orc_xy.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_int, _d, _d]
+        L.orc_sincos_cr.argtypes = [ctypes.c_int64, _d, _d, _d]
+        L.orc_edges_brute.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_int64, _i64p, _i64p]
+        L.orc_edges_brute.restype = ctypes.c_int64
+        L.orc_edges_quadtree.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p,
+                                         _i64p, ctypes.POINTER(QtTiming)]
+        L.orc_edges_quadtree.restype = ctypes.c_int64
+        L.orc_csr_from_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i64p, _i64p, _i64p]
+        _lib = L
+    return _lib
+
+
+def _p(a, t=_d):
+    return a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def philox_raw(ctr, key):
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().orc_philox_raw(c, k, o)
+    return list(o)
+
+
+def philox_uniforms(n, seed, offset=0):
+    u1 = np.empty(n, np.float64)
+    u2 = np.empty(n, np.float64)
+    lib().orc_philox_uniforms(n, seed, offset, _p(u1), _p(u2))
+    return u1, u2
+
+
+def sample_from_uniforms(u1, u2, two_over_alpha, sinh_half, r_cap, rp_cap):
+    """hrgen generator.py:160-179 on the given uniforms (libm asinh/tanh)."""
+    u1, u2 = _f64(u1), _f64(u2)
+    n = u1.size
+    phi, rn, rp = (np.empty(n, np.float64) for _ in range(3))
+    lib().orc_sample_from_uniforms(n, _p(u1), _p(u2), two_over_alpha, sinh_half, r_cap, rp_cap,
+                                   _p(phi), _p(rn), _p(rp))
+    return phi, rn, rp
+
+
+def circle_params(rp, a):
+    """hrgen geometry.py:141-157."""
+    rp = _f64(rp)
+    cr = np.empty_like(rp)
+    rad = np.empty_like(rp)
+    lib().orc_circle_params(rp.size, _p(rp), a, _p(cr), _p(rad))
+    return cr, rad
+
+
+def sincos_cr(x):
+    x = _f64(x)
+    s = np.empty_like(x)
+    c = np.empty_like(x)
+    lib().orc_sincos_cr(x.size, _p(x), _p(s), _p(c))
+    return s, c
+
+
+def edges_brute(phi, rp, a, trig=TRIG_LIBM, nthreads=0):
+    """Reference edge set {(v,w): v<w, pred(v->w)} by all-pairs tests
+    (hrgen generator.py:182-187 with the quadtree.py:611-613 predicate).
+    Returns an (m, 2) int64 array sorted lexicographically."""
+    phi, rp = _f64(phi), _f64(rp)
+    n = phi.size
+    m = lib().orc_edges_brute(n, _p(phi), _p(rp), a, trig, nthreads, 0, None, None)
+    u = np.empty(m, np.int64)
+    v = np.empty(m, np.int64)
+    lib().orc_edges_brute(n, _p(phi), _p(rp), a, trig, nthreads, m, _p(u, _i64p), _p(v, _i64p))
+    return np.column_stack((u, v))
+
+
+def edges_quadtree(phi, rp, a, alpha, max_r, capacity=512, trig=TRIG_LIBM, nthreads=0,
+                   query_lo=0, query_hi=-1, want_pairs=True):
+    """Reference edge set through the restated polar quadtree
+    (hrgen quadtree.py build/pack/query_many + generator.py:190-225).
+    Returns (pairs (m,2) or None, m, QtTiming)."""
+    phi, rp = _f64(phi), _f64(rp)
+    n = phi.size
+    tm = QtTiming()
+    if not want_pairs:
+        m = lib().orc_edges_quadtree(n, _p(phi), _p(rp), a, alpha, max_r, capacity, trig,
+                                     nthreads, query_lo, query_hi, 0, None, None,
+                                     ctypes.byref(tm))
+        if m < 0:
+            raise ValueError("point outside the tree region")
+        return None, m, tm
+    # single pass with a generous buffer, retry if it was too small
+    cap = max(1024, 64 * n)
+    while True:
+        u = np.empty(cap, np.int64)
+        v = np.empty(cap, np.int64)
+        m = lib().orc_edges_quadtree(n, _p(phi), _p(rp), a, alpha, max_r, capacity, trig,
+                                     nthreads, query_lo, query_hi, cap, _p(u, _i64p),
+                                     _p(v, _i64p), ctypes.byref(tm))
+        if m < 0:
+            raise ValueError("point outside the tree region")
+        if m <= cap:
+            return np.column_stack((u[:m], v[:m])), m, tm
+        cap = m
+
+
+def csr_from_pairs(n, pairs):
+    """hrgen graph.py:52-77 (rows sorted) for u<v pairs."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.int64).reshape(-1, 2)
+    u = np.ascontiguousarray(pairs[:, 0])
+    v = np.ascontiguousarray(pairs[:, 1])
+    m = u.size
+    indptr = np.empty(n + 1, np.int64)
+    indices = np.empty(2 * m, np.int64)
+    lib().orc_csr_from_pairs(n, m, _p(u, _i64p), _p(v, _i64p), _p(indptr, _i64p),
+                             _p(indices, _i64p))
+    return indptr, indices
+
+
+def edge_hash(pairs):
+    """sha256 of the lexicographically sorted (m,2) little-endian int64 edge
+    array -- the form hrgen Graph.edge_array() (graph.py:38-42) returns."""
+    import hashlib
+    arr = np.ascontiguousarray(pairs, dtype="<i8").reshape(-1, 2)
+    return hashlib.sha256(arr.tobytes()).hexdigest()

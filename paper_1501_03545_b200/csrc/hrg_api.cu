@@ -1,0 +1,583 @@
+// hrg_api.cu -- C ABI (include/hrgen_b200.h) over the sm_100a kernels.
+//
+// Host orchestration of one generation on one stream.  The only host<->device
+// synchronisation inside a generation is reading the CSR size after the count
+// pass (to size the index buffer); everything else is queued asynchronously.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hrgen_b200.h"
+#include "hrg_kernels.cuh"
+
+using namespace hrg;
+
+namespace {
+
+thread_local std::string g_err;
+
+hrg_status fail(hrg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(HRG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t b = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct ToI64 {
+  __host__ __device__ __forceinline__ long long operator()(const int32_t& x) const { return x; }
+};
+
+}  // namespace
+
+struct hrg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  // coordinates in vertex-id order
+  Buf phi, rn, rp;
+  // sort
+  Buf keys_in, keys_out, vals_in, vals_out;
+  // sorted SoA
+  Buf s_phi, s_px, s_py, s_cx, s_cy, s_rsq, s_rf, s_bf, s_rp, s_rn;
+  // index
+  Buf bands, dir, dir_total, bad;
+  // CSR
+  Buf deg, rowptr, idx, idx2, cand;
+  Buf temp;
+  Buf widen;
+  int64_t n = 0, nnz = 0;
+  bool have_result = false;
+  bool coords_sorted = false;  // angular order: coordinates live in s_phi/s_rn/s_rp
+  int32_t* idx_final = nullptr;
+  cudaEvent_t ev[6] = {};
+  int query_blocks_per_sm = 0;
+};
+
+namespace {
+
+hrg_status check_model(const hrg_model* m) {
+  if (!m) return fail(HRG_ERR_PARAMETER_DOMAIN, "model is NULL");
+  if (m->n < 1) return fail(HRG_ERR_PARAMETER_DOMAIN, "n must be at least 1");
+  if (m->n >= (int64_t)1 << 30) return fail(HRG_ERR_PARAMETER_DOMAIN, "n must be below 2^30");
+  if (!(m->alpha > 0.0)) return fail(HRG_ERR_PARAMETER_DOMAIN, "alpha must be positive");
+  if (!(m->R > 0.0)) return fail(HRG_ERR_PARAMETER_DOMAIN, "radius must be positive");
+  if (!(m->max_r > 0.0 && m->max_r < 1.0))
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "max_r must be in (0, 1)");  // quadtree.py:260
+  if (!(m->cosh_r_minus_1 > 0.0)) return fail(HRG_ERR_PARAMETER_DOMAIN, "bad cosh(R)-1");
+  return HRG_OK;
+}
+
+BandSpec make_bands(double R, int* L_out) {
+  BandSpec S;
+  memset(&S, 0, sizeof(S));
+  int L = kMaxBands;
+  S.L = L;
+  for (int j = 0; j < L; ++j) S.thr[j] = std::tanh(R * j / L / 2.0);
+  *L_out = L;
+  return S;
+}
+
+hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
+  size_t d = sizeof(double) * (size_t)n, f = sizeof(float) * (size_t)n, i32 = 4 * (size_t)n;
+  size_t u64 = 8 * (size_t)n;
+  CUDA_TRY(c->phi.ensure(d)); CUDA_TRY(c->rn.ensure(d)); CUDA_TRY(c->rp.ensure(d));
+  CUDA_TRY(c->keys_in.ensure(u64)); CUDA_TRY(c->keys_out.ensure(u64));
+  CUDA_TRY(c->vals_in.ensure(i32)); CUDA_TRY(c->vals_out.ensure(i32));
+  for (Buf* b : {&c->s_phi, &c->s_px, &c->s_py, &c->s_cx, &c->s_cy, &c->s_rsq, &c->s_rp, &c->s_rn})
+    CUDA_TRY(b->ensure(d));
+  CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
+  CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
+  CUDA_TRY(c->dir.ensure(4 * (size_t)(2 * n + 2 * kMaxBands + 64)));
+  CUDA_TRY(c->dir_total.ensure(8)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
+  CUDA_TRY(c->deg.ensure(i32)); CUDA_TRY(c->rowptr.ensure(8 * (size_t)(n + 1)));
+  return HRG_OK;
+}
+
+inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+double ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// Sort keys -> permutation; build the sorted SoA, band table and directory.
+hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, int L,
+                       const hrg_shard* shard, double C) {
+  int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  int end_bit = kQBits + 6;
+  size_t tb = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->keys_in.as<uint64_t>(),
+                                           c->keys_out.as<uint64_t>(), c->vals_in.as<int32_t>(),
+                                           c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
+  CUDA_TRY(c->temp.ensure(tb));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->temp.p, tb, c->keys_in.as<uint64_t>(),
+                                           c->keys_out.as<uint64_t>(), c->vals_in.as<int32_t>(),
+                                           c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
+  SoA s{c->s_phi.as<double>(), c->s_px.as<double>(), c->s_py.as<double>(), c->s_cx.as<double>(),
+        c->s_cy.as<double>(), c->s_rsq.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
+  k_gather<<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
+                                          c->rp.as<double>(), c->rn.as<double>(),
+                                          M->cosh_r_minus_1, s, c->s_rp.as<double>(),
+                                          c->s_rn.as<double>());
+  uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
+  if (shard && shard->count > 1) {
+    uint64_t span = (uint64_t)1 << kQBits;
+    qlo = ((uint64_t)shard->index * span + (uint64_t)shard->count - 1) / (uint64_t)shard->count;
+    qhi = ((uint64_t)(shard->index + 1) * span + (uint64_t)shard->count - 1) /
+          (uint64_t)shard->count;
+    if (shard->index + 1 == shard->count) qhi = span;
+  }
+  k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
+                                 c->dir_total.as<int64_t>());
+  k_band_minmax<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(),
+                                               c->s_bf.as<float>(), c->bands.as<Band>());
+  k_band_finish<<<1, 64, 0, st>>>(c->bands.as<Band>(), L);
+  k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
+                                            c->dir.as<int32_t>());
+  k_dir_tail<<<L, 256, 0, st>>>(c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
+                                c->dir.as<int32_t>());
+  CUDA_TRY(cudaGetLastError());
+  return HRG_OK;
+}
+
+// Count pass, scan, write pass (+ row sort when ids are not positions).
+hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool sample_ids,
+                      hrg_stats* stats) {
+  int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  QueryArgs A;
+  A.s = SoA{c->s_phi.as<double>(), c->s_px.as<double>(), c->s_py.as<double>(),
+            c->s_cx.as<double>(), c->s_cy.as<double>(), c->s_rsq.as<double>(),
+            c->s_rf.as<float>(), c->s_bf.as<float>()};
+  A.id = c->vals_out.as<int32_t>();
+  A.bands = c->bands.as<Band>();
+  A.dir = c->dir.as<int32_t>();
+  A.L = L;
+  A.C = C;
+  A.R_pad = nextafterf((float)M->R, INFINITY) + 3e-5f;
+  A.a_f = (float)M->cosh_r_minus_1;
+  // 2^-45 bounds the absolute fp64 error of dx*dx+dy*dy and rad^2 (all
+  // operands <= 1 in magnitude); see DESIGN.md "window padding".
+  A.E_over_tanh = (float)(std::ldexp(1.0, -45) / std::tanh(M->R)) * 1.001f;
+  A.deg = c->deg.as<int32_t>();
+  A.rowptr = c->rowptr.as<int64_t>();
+  A.out = nullptr;
+  A.cand = c->cand.as<unsigned long long>();
+
+  if (c->query_blocks_per_sm == 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_query<false, true>, 256, 0);
+    c->query_blocks_per_sm = std::max(1, nb);
+  }
+  // persistent grid: every resident warp strides over the shard's queries
+  int64_t want_warps = std::max<int64_t>(n, 1);
+  int64_t grid = std::min<int64_t>((want_warps + 7) / 8,
+                                   (int64_t)c->sm_count * c->query_blocks_per_sm);
+  grid = std::max<int64_t>(grid, 1);
+
+  CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
+  CUDA_TRY(cudaMemsetAsync(c->cand.p, 0, 8, st));
+  CUDA_TRY(cudaEventRecord(c->ev[2], st));
+  if (sample_ids) k_query<false, true><<<(unsigned)grid, 256, 0, st>>>(A);
+  else k_query<false, false><<<(unsigned)grid, 256, 0, st>>>(A);
+  CUDA_TRY(cudaEventRecord(c->ev[3], st));
+  CUDA_TRY(cudaGetLastError());
+
+  // rowptr[0] = 0, rowptr[1..n] = inclusive scan of deg
+  CUDA_TRY(cudaMemsetAsync(c->rowptr.p, 0, 8, st));
+  cub::TransformInputIterator<long long, ToI64, const int32_t*> it(c->deg.as<int32_t>(), ToI64());
+  size_t tb = 0;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, it, c->rowptr.as<long long>() + 1, (int)n, st));
+  CUDA_TRY(c->temp.ensure(tb));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(c->temp.p, tb, it, c->rowptr.as<long long>() + 1, (int)n, st));
+  int64_t nnz = 0;
+  unsigned long long cand = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&cand, c->cand.p, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (nnz >= ((int64_t)1 << 31) && sample_ids)
+    return fail(HRG_ERR_INTERNAL, "row sort supports at most 2^31-1 CSR entries");
+
+  CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
+  A.out = c->idx.as<int32_t>();
+  CUDA_TRY(cudaEventRecord(c->ev[4], st));
+  if (sample_ids) k_query<true, true><<<(unsigned)grid, 256, 0, st>>>(A);
+  else k_query<true, false><<<(unsigned)grid, 256, 0, st>>>(A);
+  CUDA_TRY(cudaEventRecord(c->ev[5], st));
+  CUDA_TRY(cudaGetLastError());
+  int launches = 2;
+  c->idx_final = c->idx.as<int32_t>();
+  if (sample_ids && nnz > 0) {
+    // rows were written in (band, angle) order of the neighbours; hrgen's
+    // Graph keeps each row sorted by id (graph.py:69-71)
+    CUDA_TRY(c->idx2.ensure(4 * (size_t)nnz));
+    size_t sb = 0;
+    const int64_t* rp = c->rowptr.as<int64_t>();
+    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, c->idx.as<int32_t>(),
+                                                c->idx2.as<int32_t>(), (int)nnz, (int)n, rp,
+                                                rp + 1, st));
+    CUDA_TRY(c->temp.ensure(sb));
+    sb = c->temp.bytes;
+    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, c->idx.as<int32_t>(),
+                                                c->idx2.as<int32_t>(), (int)nnz, (int)n, rp,
+                                                rp + 1, st));
+    c->idx_final = c->idx2.as<int32_t>();
+    launches += 1;
+  }
+  c->nnz = nnz;
+  if (stats) {
+    stats->nnz = nnz;
+    stats->m = nnz / 2;
+    stats->candidates = (int64_t)cand;
+    stats->kernel_launches += launches;
+  }
+  return HRG_OK;
+}
+
+hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* shard,
+                        bool sample_ids, bool from_coords, uint64_t seed, hrg_stats* stats) {
+  int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  int L = 0;
+  BandSpec S = make_bands(M->R, &L);
+  double C = std::ldexp(1.0, kQBits) / kTwoPi;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->n = n;
+    stats->radius = M->R;
+    stats->alpha = M->alpha;
+    stats->n_bands = L;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  if (!from_coords) {
+    SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
+    k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
+                                            c->rp.as<double>(), c->keys_in.as<uint64_t>(),
+                                            c->vals_in.as<int32_t>());
+  } else {
+    CUDA_TRY(cudaMemsetAsync(c->bad.p, 0, 4, st));
+    k_keys_from_coords<<<blocks_for(n), 256, 0, st>>>(
+        n, c->phi.as<double>(), c->rp.as<double>(), M->max_r, C, S, c->rn.as<double>(),
+        c->keys_in.as<uint64_t>(), c->vals_in.as<int32_t>(), c->bad.as<int>());
+    int bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, c->bad.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (bad) return fail(HRG_ERR_OUT_OF_BOUNDS, "point outside the tree region");
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  hrg_status s = build_index(c, M, S, L, shard, C);
+  if (s != HRG_OK) return s;
+  if (stats) stats->kernel_launches = 8;  // sample/keys, sort, gather, 5 index kernels
+  s = emit_edges(c, M, L, C, sample_ids, stats);
+  if (s != HRG_OK) return s;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  c->n = n;
+  c->have_result = true;
+  c->coords_sorted = !sample_ids;
+  if (stats) {
+    stats->t_sample_ms = ev_ms(c->ev[0], c->ev[1]);
+    stats->t_build_ms = ev_ms(c->ev[1], c->ev[2]);
+    stats->t_edges_ms = ev_ms(c->ev[2], c->ev[5]);
+    stats->t_query_count_ms = ev_ms(c->ev[2], c->ev[3]);
+    stats->t_query_write_ms = ev_ms(c->ev[4], c->ev[5]);
+  }
+  return HRG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hrg_version(void) { return "hrgen_b200 1 (sm_100a)"; }
+const char* hrg_last_error(void) { return g_err.c_str(); }
+
+hrg_status hrg_context_create(int device, void* cuda_stream, hrg_context** out) {
+  if (!out) return fail(HRG_ERR_PARAMETER_DOMAIN, "out is NULL");
+  CUDA_TRY(cudaSetDevice(device));
+  hrg_context* c = new hrg_context();
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  for (auto& e : c->ev) {
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
+  }
+  *out = c;
+  return HRG_OK;
+}
+
+hrg_status hrg_context_destroy(hrg_context* c) {
+  if (!c) return HRG_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
+                 &c->s_phi, &c->s_px, &c->s_py, &c->s_cx, &c->s_cy, &c->s_rsq, &c->s_rf,
+                 &c->s_bf, &c->s_rp, &c->s_rn, &c->bands, &c->dir, &c->dir_total, &c->bad,
+                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
+    b->release();
+  for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  delete c;
+  return HRG_OK;
+}
+
+hrg_status hrg_context_set_stream(hrg_context* c, void* s) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  c->stream = (cudaStream_t)s;
+  return HRG_OK;
+}
+
+hrg_status hrg_expected_avg_degree(int64_t n, double alpha, double radius, double* out) {
+  // hrgen geometry.py:170-190
+  if (!(alpha > 0.5)) return fail(HRG_ERR_PARAMETER_DOMAIN, "alpha must be > 0.5");
+  if (!(radius > 0.0)) return fail(HRG_ERR_PARAMETER_DOMAIN, "radius must be > 0");
+  if (n < 1) return fail(HRG_ERR_PARAMETER_DOMAIN, "n must be >= 1");
+  const double pi = 3.141592653589793;
+  double xi = alpha / (alpha - 0.5);
+  double inner = alpha * (radius / 2.0) *
+                     ((pi / 4.0) / (alpha * alpha) - (pi - 1.0) / alpha + (pi - 2.0)) - 1.0;
+  *out = (2.0 / pi) * xi * xi * (double)n *
+         (std::exp(-radius / 2.0) + std::exp(-alpha * radius) * inner);
+  return HRG_OK;
+}
+
+hrg_status hrg_target_radius(int64_t n, double k, double alpha, double rel_tol, double* out) {
+  // hrgen geometry.py:197-232 (geometric grid, peak, bisection on the decaying branch)
+  if (!(alpha > 0.5)) return fail(HRG_ERR_PARAMETER_DOMAIN, "alpha must be > 0.5");
+  if (!(k > 0.0 && k < (double)(n - 1)))
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "target average degree must be in (0, n-1)");
+  const double lo_r = 1e-6, hi_r = 200.0;
+  double best = -INFINITY, lo = lo_r;
+  for (int i = 0; i < 512; ++i) {
+    double r = std::pow(10.0, std::log10(lo_r) + (std::log10(hi_r) - std::log10(lo_r)) * i / 511.0);
+    if (i == 0) r = lo_r;
+    if (i == 511) r = hi_r;
+    double v;
+    hrg_expected_avg_degree(n, alpha, r, &v);
+    if (v > best) { best = v; lo = r; }
+  }
+  double hi = hi_r, vhi;
+  hrg_expected_avg_degree(n, alpha, hi, &vhi);
+  if (best < k || vhi > k) return fail(HRG_ERR_INFEASIBLE, "no radius yields that average degree");
+  for (int it = 0; it < 200; ++it) {
+    double mid = 0.5 * (lo + hi), v;
+    hrg_expected_avg_degree(n, alpha, mid, &v);
+    if (std::fabs(v - k) <= rel_tol * k) { *out = mid; return HRG_OK; }
+    if (v > k) lo = mid; else hi = mid;
+  }
+  return fail(HRG_ERR_INFEASIBLE, "bisection failed to reach tolerance");
+}
+
+hrg_status hrg_model_init(int64_t n, double alpha, double R, hrg_model* out) {
+  if (!out) return fail(HRG_ERR_PARAMETER_DOMAIN, "out is NULL");
+  out->n = n;
+  out->alpha = alpha;
+  out->R = R;
+  double s = std::sinh(R / 2.0);
+  out->cosh_r_minus_1 = 2.0 * (s * s);
+  out->max_r = std::tanh(R / 2.0);
+  out->rp_cap = std::nextafter(out->max_r, 0.0);
+  out->r_cap = std::nextafter(R, 0.0);
+  out->two_over_alpha = 2.0 / alpha;
+  out->sinh_half_alpha_r = std::sinh(alpha * R / 2.0);
+  return check_model(out);
+}
+
+hrg_status hrg_generate(hrg_context* c, const hrg_model* M, uint64_t seed, int order,
+                        const hrg_shard* shard, hrg_stats* stats) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  hrg_status s = check_model(M);
+  if (s != HRG_OK) return s;
+  if (order != HRG_ORDER_SAMPLE && order != HRG_ORDER_ANGULAR)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "unknown vertex order");
+  if (shard && (shard->count < 1 || shard->index < 0 || shard->index >= shard->count))
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "bad shard");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->have_result = false;
+  s = ensure_point_buffers(c, M->n);
+  if (s != HRG_OK) return s;
+  return run_pipeline(c, M, shard, order == HRG_ORDER_SAMPLE, false, seed, stats);
+}
+
+hrg_status hrg_sample_points(hrg_context* c, const hrg_model* M, uint64_t seed, int order,
+                             int mem_kind, double* phi, double* rn, double* rp) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  hrg_status s = check_model(M);
+  if (s != HRG_OK) return s;
+  if (order != HRG_ORDER_SAMPLE && order != HRG_ORDER_ANGULAR)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "unknown vertex order");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->have_result = false;
+  s = ensure_point_buffers(c, M->n);
+  if (s != HRG_OK) return s;
+  int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  int L = 0;
+  BandSpec S = make_bands(M->R, &L);
+  double C = std::ldexp(1.0, kQBits) / kTwoPi;
+  SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
+  k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
+                                          c->rp.as<double>(), c->keys_in.as<uint64_t>(),
+                                          c->vals_in.as<int32_t>());
+  CUDA_TRY(cudaGetLastError());
+  const double *sp = c->phi.as<double>(), *sn = c->rn.as<double>(), *sr = c->rp.as<double>();
+  if (order == HRG_ORDER_ANGULAR) {
+    s = build_index(c, M, S, L, nullptr, C);
+    if (s != HRG_OK) return s;
+    sp = c->s_phi.as<double>(); sn = c->s_rn.as<double>(); sr = c->s_rp.as<double>();
+  }
+  cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  size_t d = sizeof(double) * (size_t)n;
+  if (phi) CUDA_TRY(cudaMemcpyAsync(phi, sp, d, k, st));
+  if (rn) CUDA_TRY(cudaMemcpyAsync(rn, sn, d, k, st));
+  if (rp) CUDA_TRY(cudaMemcpyAsync(rp, sr, d, k, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HRG_OK;
+}
+
+hrg_status hrg_edges_from_coords(hrg_context* c, const hrg_model* M, const double* phi,
+                                 const double* rp, int mem_kind, const hrg_shard* shard,
+                                 hrg_stats* stats) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  hrg_status s = check_model(M);
+  if (s != HRG_OK) return s;
+  if (!phi || !rp) return fail(HRG_ERR_PARAMETER_DOMAIN, "coordinate pointer is NULL");
+  if (shard && (shard->count < 1 || shard->index < 0 || shard->index >= shard->count))
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "bad shard");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->have_result = false;
+  s = ensure_point_buffers(c, M->n);
+  if (s != HRG_OK) return s;
+  cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_TRY(cudaMemcpyAsync(c->phi.p, phi, sizeof(double) * M->n, k, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->rp.p, rp, sizeof(double) * M->n, k, c->stream));
+  return run_pipeline(c, M, shard, true, true, 0, stats);
+}
+
+hrg_status hrg_result_sizes(hrg_context* c, int64_t* n, int64_t* nnz) {
+  if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
+  if (n) *n = c->n;
+  if (nnz) *nnz = c->nnz;
+  return HRG_OK;
+}
+
+hrg_status hrg_result_device_ptrs(hrg_context* c, const double** phi, const double** rn,
+                                  const double** rp, const int64_t** indptr,
+                                  const int32_t** indices) {
+  if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
+  if (phi) *phi = c->coords_sorted ? c->s_phi.as<double>() : c->phi.as<double>();
+  if (rn) *rn = c->coords_sorted ? c->s_rn.as<double>() : c->rn.as<double>();
+  if (rp) *rp = c->coords_sorted ? c->s_rp.as<double>() : c->rp.as<double>();
+  if (indptr) *indptr = c->rowptr.as<int64_t>();
+  if (indices) *indices = c->idx_final;
+  return HRG_OK;
+}
+
+hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn, double* rp,
+                           int64_t* indptr, void* indices, int index_bytes) {
+  if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
+  if (indices && index_bytes != 4 && index_bytes != 8)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "index_bytes must be 4 or 8");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  size_t d = sizeof(double) * (size_t)c->n;
+  const double *sp, *sn, *sr;
+  hrg_result_device_ptrs(c, &sp, &sn, &sr, nullptr, nullptr);
+  if (phi) CUDA_TRY(cudaMemcpyAsync(phi, sp, d, k, st));
+  if (rn) CUDA_TRY(cudaMemcpyAsync(rn, sn, d, k, st));
+  if (rp) CUDA_TRY(cudaMemcpyAsync(rp, sr, d, k, st));
+  if (indptr) CUDA_TRY(cudaMemcpyAsync(indptr, c->rowptr.p, 8 * (size_t)(c->n + 1), k, st));
+  if (indices && c->nnz > 0) {
+    if (index_bytes == 4) {
+      CUDA_TRY(cudaMemcpyAsync(indices, c->idx_final, 4 * (size_t)c->nnz, k, st));
+    } else {
+      // widen on the device in chunks, copy each chunk out
+      const int64_t chunk = (int64_t)1 << 25;
+      CUDA_TRY(c->widen.ensure(8 * (size_t)std::min<int64_t>(chunk, c->nnz)));
+      for (int64_t off = 0; off < c->nnz; off += chunk) {
+        int64_t len = std::min<int64_t>(chunk, c->nnz - off);
+        k_widen<<<blocks_for(len), 256, 0, st>>>(len, c->idx_final + off, c->widen.as<int64_t>());
+        CUDA_TRY(cudaMemcpyAsync((int64_t*)indices + off, c->widen.p, 8 * (size_t)len, k, st));
+      }
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return HRG_OK;
+}
+
+hrg_status hrg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(HRG_ERR_PARAMETER_DOMAIN, "out is NULL");
+  CUDA_TRY(cudaMallocHost(out, std::max<size_t>(bytes, 1)));
+  return HRG_OK;
+}
+
+hrg_status hrg_host_free(void* p) {
+  if (p) CUDA_TRY(cudaFreeHost(p));
+  return HRG_OK;
+}
+
+hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, double* s, double* co) {
+  if (!c || n < 0 || !x || !s || !co) return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
+  if (n == 0) return HRG_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  Buf b;
+  CUDA_TRY(b.ensure(24 * (size_t)n));
+  double* d = b.as<double>();
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemcpyAsync(d, x, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+  k_sincos<<<blocks_for(n), 256, 0, st>>>(n, d, d + n, d + 2 * n);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(s, d + n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(co, d + 2 * n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  b.release();
+  return HRG_OK;
+}
+
+hrg_status hrg_synchronize(hrg_context* c) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return HRG_OK;
+}
+
+}  // extern "C"

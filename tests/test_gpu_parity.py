@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path against the reference (golden fixtures) and the
+CPU oracle, through the C ABI.  Integer/index results must be bit-exact;
+sampled radii (libm vs CUDA asinh/tanh) are compared within a stated ulp
+tolerance.  Run on a B200: pytest -m gpu."""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_data as gd
+import paper_1501_03545_b200 as P
+from paper_1501_03545_b200 import GeneratorParams, Graph, VertexCoordinates
+
+pytestmark = pytest.mark.gpu
+
+RUNS = gd.runs()
+
+
+def edge_set_hash(oracle, g: Graph):
+    return oracle.edge_hash(g.edge_array())
+
+
+def check_csr(g: Graph):
+    """hrgen Graph invariants: symmetric, rows strictly increasing, no loops."""
+    ip, ix = np.asarray(g.indptr), np.asarray(g.indices)
+    n = ip.size - 1
+    assert ip[0] == 0 and np.all(np.diff(ip) >= 0) and ip[-1] == ix.size
+    if ix.size == 0:
+        return
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ip))
+    assert ix.min() >= 0 and ix.max() < n
+    assert not np.any(ix == rows)
+    inner = np.ones(ix.size - 1, bool)
+    starts = ip[1:-1]
+    starts = starts[(starts > 0) & (starts < ix.size)]
+    inner[starts - 1] = False
+    assert np.all(ix[1:][inner] > ix[:-1][inner])
+    # symmetry: a random 64-bit multiplicative hash of (row, col) summed over
+    # all entries equals the same over (col, row)
+    rng = np.random.default_rng(1)
+    h1 = rng.integers(1, 2**62, n, dtype=np.int64).astype(np.uint64)
+    h2 = rng.integers(1, 2**62, n, dtype=np.int64).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        a = np.sum(h1[rows] * h2[ix], dtype=np.uint64)
+        b = np.sum(h1[ix] * h2[rows], dtype=np.uint64)
+    assert a == b
+
+
+# ---------------------------------------------------------------- arithmetic
+def test_device_sincos_is_correctly_rounded(oracle):
+    eng = P.get_engine()
+    rng = np.random.default_rng(0)
+    x = np.concatenate([
+        rng.random(2_000_000) * 2 * math.pi,
+        np.array([0.0, 5e-324, 1e-300, 1e-8, math.pi / 4, math.pi / 2, math.pi,
+                  3 * math.pi / 2, np.nextafter(2 * math.pi, 0.0)]),
+        math.pi / 2 + (rng.random(10000) - 0.5) * 1e-9,
+        math.pi + (rng.random(10000) - 0.5) * 1e-12,
+        2 * math.pi - rng.random(10000) * 1e-10,
+    ])
+    s, c = eng.debug_sincos(x)
+    s_ref, c_ref = oracle.sincos_cr(x)
+    assert np.array_equal(s, s_ref)
+    assert np.array_equal(c, c_ref)
+
+
+def test_sampler_matches_oracle(oracle):
+    """Philox uniforms bit-exact (phi = 2pi*u1 is one multiply); radii from
+    CUDA asinh/tanh within 4 ulp of libm's."""
+    n, alpha, R, seed = 200_000, 0.75, 28.789361743909193, 2
+    co = P.sample_points(n, alpha, R, seed)
+    u1, u2 = oracle.philox_uniforms(n, seed)
+    k = P.model_constants(R, alpha)
+    phi, rn, rp = oracle.sample_from_uniforms(u1, u2, k["two_over_alpha"],
+                                             k["sinh_half_alpha_r"], k["r_cap"], k["rp_cap"])
+    assert np.array_equal(co.phi, phi)
+    assert np.all(np.abs(co.r_native - rn) <= 4 * np.spacing(rn))
+    assert np.all(np.abs(co.r_poincare - rp) <= 4 * np.spacing(rp))
+    assert co.r_native.max() < R and co.r_poincare.max() < k["max_r"]
+
+
+def test_sampled_distributions_fit():
+    # hrgen tests/test_generator.py:107-116
+    from scipy import stats
+    alpha, R = 0.7, 16.0
+    co = P.sample_points(40_000, alpha, R, seed=123)
+    assert stats.kstest(co.phi / (2 * math.pi), "uniform").pvalue > 0.01
+    cdf = lambda r: (np.cosh(alpha * r) - 1.0) / (math.cosh(alpha * R) - 1.0)  # noqa: E731
+    assert stats.kstest(co.r_native, cdf).pvalue > 0.01
+
+
+def test_sample_points_deterministic_and_in_range():
+    a = P.sample_points(5000, 0.8, 14.0, seed=42)
+    b = P.sample_points(5000, 0.8, 14.0, seed=42)
+    c = P.sample_points(5000, 0.8, 14.0, seed=43)
+    assert np.array_equal(a.phi, b.phi) and np.array_equal(a.r_poincare, b.r_poincare)
+    assert not np.array_equal(a.phi, c.phi)
+    assert a.phi.min() >= 0.0 and a.phi.max() < 2 * math.pi
+    assert a.r_native.max() < 14.0 and a.r_poincare.max() < 1.0
+
+
+# ---------------------------------------------------- reference edge sets
+@pytest.mark.parametrize("run", RUNS, ids=lambda r: f"{r.tag}-n{r.n}-s{r.seed}-R{r.R:.2f}")
+def test_reference_runs_bit_exact(oracle, run):
+    """On hrgen's own coordinates the GPU edge set IS hrgen's (sha256)."""
+    coords = VertexCoordinates(phi=run.phi, r_native=None, r_poincare=run.r_poincare)
+    g = P.edges_from_coordinates(coords, run.R, alpha=run.alpha)
+    assert g.m == run.m
+    assert edge_set_hash(oracle, g) == run.edge_sha256
+    check_csr(g)
+
+
+def test_config0_edges_exact():
+    run = gd.runs(["config0"])[0]
+    coords = VertexCoordinates(phi=run.phi, r_native=None, r_poincare=run.r_poincare)
+    g = P.edges_from_coordinates(coords, run.R)
+    assert np.array_equal(g.edge_array(), gd.config0_edges())
+
+
+# ------------------------------------------------------ generated graphs
+GEN_CASES = [
+    dict(n=100_000, avg_degree=10.0, gamma=3.0, seed=1),
+    dict(n=60_000, avg_degree=32.0, gamma=2.5, seed=2),
+    dict(n=50_000, avg_degree=4.0, gamma=2.2, seed=4),
+    dict(n=20_000, avg_degree=256.0, gamma=5.0, seed=4),
+    dict(n=100_000, radius=33.165607448498854, alpha=1.0, seed=3),
+    dict(n=100_000, radius=35.50799080982715, alpha=0.6, seed=4),
+]
+
+
+@pytest.mark.parametrize("kw", GEN_CASES, ids=lambda k: "-".join(f"{a}{b}" for a, b in k.items()))
+def test_generate_matches_oracle(oracle, kw):
+    """generate() == oracle quadtree on the GPU's own coordinates.  Against
+    the CR-trig oracle (the same cos/sin values) the match is exact; against
+    libm trig (hrgen's own arithmetic) any difference must be a pair whose
+    decision sits on a 1-ulp cos/sin difference -- counted and reported."""
+    p = GeneratorParams(**kw)
+    model = p.resolve()
+    g, st = P.generate_with_stats(p)
+    check_csr(g)
+    co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e_cr, m_cr, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                          P.to_poincare_radius(model.R), 512, oracle.TRIG_CR)
+    assert g.m == m_cr
+    assert edge_set_hash(oracle, g) == oracle.edge_hash(e_cr)
+    e_lm, m_lm, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                          P.to_poincare_radius(model.R), 512, oracle.TRIG_LIBM)
+    s_cr = set(map(tuple, e_cr.tolist()))
+    s_lm = set(map(tuple, e_lm.tolist()))
+    diff = s_cr ^ s_lm
+    print(f"[parity] {kw}: m={g.m} candidates={st.candidates} "
+          f"libm-vs-CR mismatches={len(diff)}")
+    assert len(diff) <= max(2, g.m // 1_000_000)
+
+
+def test_config1_full_size_matches_oracle(oracle):
+    """BASELINE config 1 (n=1e6, k=10, gamma=3, seed 1) end to end."""
+    p = GeneratorParams(n=1_000_000, avg_degree=10.0, gamma=3.0, seed=1)
+    model = p.resolve()
+    g = P.generate(p)
+    co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                    P.to_poincare_radius(model.R), 512, oracle.TRIG_CR)
+    assert g.m == m
+    assert edge_set_hash(oracle, g) == oracle.edge_hash(e)
+    assert 2 * g.m / model.n == pytest.approx(10.0, rel=0.1)
+
+
+def test_angular_order_is_a_relabelling(oracle):
+    kw = dict(n=50_000, avg_degree=16.0, gamma=2.5, seed=7)
+    gs = P.generate(GeneratorParams(**kw))
+    ga = P.generate(GeneratorParams(**kw, vertex_order="angular"))
+    check_csr(ga)
+    cs = P.sample_points(50_000, 0.75, GeneratorParams(**kw).resolve().R, 7)
+    ca = P.sample_points(50_000, 0.75, GeneratorParams(**kw).resolve().R, 7,
+                         vertex_order="angular")
+    pos = {(p, r): i for i, (p, r) in enumerate(zip(cs.phi.tolist(), cs.r_poincare.tolist()))}
+    perm = np.array([pos[(p, r)] for p, r in zip(ca.phi.tolist(), ca.r_poincare.tolist())])
+    ea = ga.edge_array()
+    mapped = np.sort(np.column_stack((perm[ea[:, 0]], perm[ea[:, 1]])), axis=1)
+    mapped = mapped[np.lexsort((mapped[:, 1], mapped[:, 0]))]
+    assert np.array_equal(mapped, gs.edge_array())
+
+
+def test_shards_partition_the_rows():
+    p = GeneratorParams(n=200_000, avg_degree=16.0, gamma=2.5, seed=9)
+    full = P.generate(p)
+    acc_rows = np.zeros(full.n, np.int64)
+    parts = []
+    for k in range(4):
+        g, st = P.generate_with_stats(p, shard=P.Shard(k, 4))
+        deg = np.diff(g.indptr)
+        assert np.all(acc_rows[deg > 0] == 0)   # disjoint row sets
+        acc_rows += deg
+        parts.append(g)
+    assert np.array_equal(acc_rows, np.diff(full.indptr))
+    for g in parts:
+        for v in np.flatnonzero(np.diff(g.indptr))[:2000]:
+            assert np.array_equal(g.neighbors(v), full.neighbors(v))
+
+
+# ------------------------------------------------------------ properties
+def test_full_size_config2_properties():
+    """BASELINE config 2 (n=1e7, k=32, gamma=2.5, seed 2): hrgen Graph
+    invariants and the realised degree at full size."""
+    p = GeneratorParams(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2)
+    g, st = P.generate_with_stats(p)
+    check_csr(g)
+    assert 2 * g.m / p.n == pytest.approx(32.0, rel=0.12)
+    print(f"[config2] m={g.m} candidates={st.candidates} "
+          f"t_sample={st.t_sample_ns/1e6:.2f}ms t_build={st.t_build_ns/1e6:.2f}ms "
+          f"t_edges={st.t_edges_ns/1e6:.2f}ms")
+
+
+def test_realized_degree_tracks_target():
+    # hrgen tests/test_generator.py:177-185
+    for alpha, kbar in ((1.0, 16.0), (1.5, 8.0)):
+        g = P.generate(GeneratorParams(n=50_000, avg_degree=kbar, alpha=alpha, seed=1))
+        assert 2.0 * g.m / 50_000 == pytest.approx(kbar, rel=0.05)
+
+
+def test_determinism_and_invariance():
+    base = dict(n=25_000, avg_degree=12.0, gamma=2.8, seed=4)
+    g1 = P.generate(GeneratorParams(**base, threads=1, leaf_capacity=32))
+    g2 = P.generate(GeneratorParams(**base, threads=3, leaf_capacity=2048))
+    assert np.array_equal(g1.indptr, g2.indptr) and np.array_equal(g1.indices, g2.indices)
+    g3 = P.generate(GeneratorParams(**{**base, "seed": 5}))
+    assert not np.array_equal(g1.indices, g3.indices)
+
+
+# ------------------------------------------------------------ edge cases
+def test_single_vertex_and_tiny_graphs():
+    g = P.generate(GeneratorParams(n=1, radius=5.0, alpha=1.0, seed=0))
+    assert g.n == 1 and g.m == 0
+    g = P.generate(GeneratorParams(n=2, radius=0.5, alpha=1.0, seed=0))
+    assert g.n == 2 and g.m == 1
+
+
+def test_degenerate_coordinates(oracle):
+    """Duplicates, the origin, angles 0 and just below 2pi, rim points."""
+    R = 12.0
+    max_r = P.to_poincare_radius(R)
+    rim = np.nextafter(max_r, 0.0)
+    phi = np.array([0.0, 0.0, 1.0, 1.0, 1.0, np.nextafter(2 * math.pi, 0), 3.0, 3.0 + 1e-15,
+                    math.pi, 0.5])
+    rp = np.array([0.0, 0.5, 0.9, 0.9, 0.9, rim, rim, rim, 0.9999, 1e-300])
+    coords = VertexCoordinates(phi=phi, r_native=None, r_poincare=rp)
+    g = P.edges_from_coordinates(coords, R)
+    a = P.model_constants(R, 1.0)["cosh_r_minus_1"]
+    want = oracle.edges_brute(phi, rp, a)
+    assert np.array_equal(g.edge_array(), want)
+
+
+def test_random_coordinates_many_radii(oracle):
+    rng = np.random.default_rng(3)
+    for R in (0.3, 2.0, 9.0, 20.0, 30.0, 37.0):
+        n = 3000
+        max_r = P.to_poincare_radius(R)
+        phi = rng.random(n) * 2 * math.pi
+        rp = np.minimum(np.sqrt(rng.random(n)) * max_r, np.nextafter(max_r, 0))
+        rp[: n // 3] = np.nextafter(max_r, 0) - rng.integers(0, 8, n // 3) * np.spacing(max_r)
+        rp = np.minimum(rp, np.nextafter(max_r, 0))
+        a = P.model_constants(R, 1.0)["cosh_r_minus_1"]
+        want = oracle.edges_brute(phi, rp, a, oracle.TRIG_CR)
+        g = P.edges_from_coordinates(VertexCoordinates(phi, None, rp), R)
+        assert np.array_equal(g.edge_array(), want), R
+
+
+def test_out_of_bounds_coordinates_raise():
+    R = 10.0
+    with pytest.raises(P.OutOfBoundsError):
+        P.edges_from_coordinates(VertexCoordinates(np.array([0.0]), None, np.array([0.9999])), R)
+    with pytest.raises(P.OutOfBoundsError):
+        P.edges_from_coordinates(VertexCoordinates(np.array([-0.1]), None, np.array([0.5])), R)
+    with pytest.raises(P.OutOfBoundsError):
+        P.edges_from_coordinates(VertexCoordinates(np.array([2 * math.pi]), None,
+                                                   np.array([0.5])), R)
+    with pytest.raises(ValueError):
+        P.generate(GeneratorParams(n=10, radius=80.0, alpha=1.0))
+
+
+def test_device_csr_tensors():
+    import torch
+    eng = P.get_engine()
+    g = P.generate(GeneratorParams(n=20_000, avg_degree=8.0, gamma=3.0, seed=1))
+    ip, ix = eng.device_csr()
+    assert ip.is_cuda and ix.dtype == torch.int32
+    assert np.array_equal(ip.cpu().numpy(), g.indptr)
+    assert np.array_equal(ix.cpu().numpy().astype(np.int64), g.indices)
