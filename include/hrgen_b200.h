@@ -74,10 +74,13 @@ typedef struct { int32_t index, count; } hrg_shard;
 typedef struct {
   int64_t n, m;            /* vertices, undirected edges (over all rows emitted) */
   int64_t nnz;             /* CSR entries emitted = sum of emitted row lengths */
-  int64_t candidates;      /* pair tests performed by the count pass */
+  int64_t candidates;      /* pair tests performed by the range query */
   double radius, alpha;
-  double t_sample_ms, t_build_ms, t_edges_ms;   /* CUDA-event phase times */
-  double t_query_count_ms, t_query_write_ms;    /* the two range-query launches */
+  int64_t heavy_queries, heavy_chunks;  /* hub queries split across warps */
+  /* CUDA-event phase times: sample | build (key sort + records + index) |
+   * edges (light query, heavy query, compaction, row ordering) */
+  double t_sample_ms, t_build_ms, t_edges_ms;
+  double t_sort_ms, t_light_ms, t_heavy_ms, t_compact_ms, t_rowsort_ms;
   int32_t n_bands;
   int32_t kernel_launches;
 } hrg_stats;

@@ -58,9 +58,12 @@ class Stats(ctypes.Structure):
     _fields_ = [
         ("n", ctypes.c_int64), ("m", ctypes.c_int64), ("nnz", ctypes.c_int64),
         ("candidates", ctypes.c_int64), ("radius", ctypes.c_double), ("alpha", ctypes.c_double),
+        ("heavy_queries", ctypes.c_int64), ("heavy_chunks", ctypes.c_int64),
         ("t_sample_ms", ctypes.c_double), ("t_build_ms", ctypes.c_double),
-        ("t_edges_ms", ctypes.c_double), ("t_query_count_ms", ctypes.c_double),
-        ("t_query_write_ms", ctypes.c_double), ("n_bands", ctypes.c_int32),
+        ("t_edges_ms", ctypes.c_double), ("t_sort_ms", ctypes.c_double),
+        ("t_light_ms", ctypes.c_double), ("t_heavy_ms", ctypes.c_double),
+        ("t_compact_ms", ctypes.c_double), ("t_rowsort_ms", ctypes.c_double),
+        ("n_bands", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
     ]
 

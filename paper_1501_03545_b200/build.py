@@ -38,6 +38,8 @@ def build(force=False, verbose=False):
     if not force and not needs_build():
         return LIB
     cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+    if os.path.exists(LIB):
+        os.unlink(LIB)  # a failed build must not leave a stale library behind
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -72,8 +72,12 @@ struct hrg_context {
   Buf phi, rn, rp;
   // sort
   Buf keys_in, keys_out, vals_in, vals_out;
-  // sorted SoA
-  Buf s_phi, s_px, s_py, s_cx, s_cy, s_rsq, s_rf, s_bf, s_rp, s_rn;
+  // sorted records
+  Buf rec, s_phi, s_rf, s_bf, s_rp, s_rn;
+  // staging + heavy queries
+  Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
+      chunk_off, seg_b, seg_e;
+  int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad;
   // CSR
@@ -84,11 +88,15 @@ struct hrg_context {
   bool have_result = false;
   bool coords_sorted = false;  // angular order: coordinates live in s_phi/s_rn/s_rp
   int32_t* idx_final = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
+  int grid_light = 0, grid_heavy = 0, grid_compact = 0;
 };
 
 namespace {
+
+enum Ev { E_START, E_SAMPLED, E_SORTED, E_INDEXED, E_PLANNED, E_COUNTED, E_WRITE0, E_WRITTEN,
+          E_ROWSORTED };
 
 hrg_status check_model(const hrg_model* m) {
   if (!m) return fail(HRG_ERR_PARAMETER_DOMAIN, "model is NULL");
@@ -118,8 +126,11 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->phi.ensure(d)); CUDA_TRY(c->rn.ensure(d)); CUDA_TRY(c->rp.ensure(d));
   CUDA_TRY(c->keys_in.ensure(u64)); CUDA_TRY(c->keys_out.ensure(u64));
   CUDA_TRY(c->vals_in.ensure(i32)); CUDA_TRY(c->vals_out.ensure(i32));
-  for (Buf* b : {&c->s_phi, &c->s_px, &c->s_py, &c->s_cx, &c->s_cy, &c->s_rsq, &c->s_rp, &c->s_rn})
-    CUDA_TRY(b->ensure(d));
+  for (Buf* b : {&c->s_phi, &c->s_rp, &c->s_rn}) CUDA_TRY(b->ensure(d));
+  CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
+  CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(64));
+  CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
+  CUDA_TRY(c->heavy_of.ensure(i32));
   CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
   CUDA_TRY(c->dir.ensure(4 * (size_t)(2 * n + 2 * kMaxBands + 64)));
@@ -151,12 +162,12 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->temp.p, tb, c->keys_in.as<uint64_t>(),
                                            c->keys_out.as<uint64_t>(), c->vals_in.as<int32_t>(),
                                            c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
-  SoA s{c->s_phi.as<double>(), c->s_px.as<double>(), c->s_py.as<double>(), c->s_cx.as<double>(),
-        c->s_cy.as<double>(), c->s_rsq.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
+  CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
+  QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
   k_gather<<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
                                           c->rp.as<double>(), c->rn.as<double>(),
-                                          M->cosh_r_minus_1, s, c->s_rp.as<double>(),
-                                          c->s_rn.as<double>());
+                                          M->cosh_r_minus_1, c->rec.as<Rec>(), q,
+                                          c->s_rp.as<double>(), c->s_rn.as<double>());
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     uint64_t span = (uint64_t)1 << kQBits;
@@ -178,18 +189,40 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   return HRG_OK;
 }
 
-// Count pass, scan, write pass (+ row sort when ids are not positions).
+template <class K>
+int occupancy_grid(hrg_context* c, K kernel, int threads = 256) {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0);
+  return std::max(1, nb) * c->sm_count;
+}
+
+// inclusive scan of int32 in[0..n) into out[1..n], out[0] = 0 (int64)
+hrg_status scan_i32_to_i64(hrg_context* c, const int32_t* in, int64_t* out, int64_t n) {
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemsetAsync(out, 0, 8, st));
+  if (n == 0) return HRG_OK;
+  cub::TransformInputIterator<long long, ToI64, const int32_t*> it(in, ToI64());
+  size_t tb = 0;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, it, (long long*)out + 1, (int)n, st));
+  CUDA_TRY(c->temp.ensure(tb));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(c->temp.p, tb, it, (long long*)out + 1, (int)n, st));
+  return HRG_OK;
+}
+
+// Light query pass, heavy (hub) pass, scans, compaction (+ row sort when ids
+// are not positions).
 hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool sample_ids,
                       hrg_stats* stats) {
   int64_t n = M->n;
   cudaStream_t st = c->stream;
   QueryArgs A;
-  A.s = SoA{c->s_phi.as<double>(), c->s_px.as<double>(), c->s_py.as<double>(),
-            c->s_cx.as<double>(), c->s_cy.as<double>(), c->s_rsq.as<double>(),
-            c->s_rf.as<float>(), c->s_bf.as<float>()};
-  A.id = c->vals_out.as<int32_t>();
+  memset(&A, 0, sizeof(A));
+  A.rec = c->rec.as<Rec>();
+  A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
   A.bands = c->bands.as<Band>();
   A.dir = c->dir.as<int32_t>();
+  A.keys = c->keys_out.as<uint64_t>();
   A.L = L;
   A.C = C;
   A.R_pad = nextafterf((float)M->R, INFINITY) + 3e-5f;
@@ -197,77 +230,132 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   // 2^-45 bounds the absolute fp64 error of dx*dx+dy*dy and rad^2 (all
   // operands <= 1 in magnitude); see DESIGN.md "window padding".
   A.E_over_tanh = (float)(std::ldexp(1.0, -45) / std::tanh(M->R)) * 1.001f;
+  A.bump = c->counters.as<unsigned long long>();
+  A.cand_total = c->counters.as<unsigned long long>() + 1;
+  A.heavy_n = reinterpret_cast<unsigned*>(c->counters.as<unsigned long long>() + 2);
+  A.overflow = reinterpret_cast<int*>(c->counters.as<unsigned long long>() + 3);
+  A.stage_off = c->stage_off.as<int64_t>();
+  A.heavy_v = c->heavy_v.as<int32_t>();
+  A.heavy_c = c->heavy_c.as<int32_t>();
+  A.heavy_of = c->heavy_of.as<int32_t>();
   A.deg = c->deg.as<int32_t>();
-  A.rowptr = c->rowptr.as<int64_t>();
-  A.out = nullptr;
-  A.cand = c->cand.as<unsigned long long>();
 
-  if (c->query_blocks_per_sm == 0) {
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_query<false, true>, 256, 0);
-    c->query_blocks_per_sm = std::max(1, nb);
+  if (c->grid_light == 0) {
+    c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
+    c->grid_heavy = occupancy_grid(c, k_heavy<true>);
+    c->grid_compact = occupancy_grid(c, k_compact_light<true>);
   }
-  // persistent grid: every resident warp strides over the shard's queries
-  int64_t want_warps = std::max<int64_t>(n, 1);
-  int64_t grid = std::min<int64_t>((want_warps + 7) / 8,
-                                   (int64_t)c->sm_count * c->query_blocks_per_sm);
-  grid = std::max<int64_t>(grid, 1);
-
-  CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
-  CUDA_TRY(cudaMemsetAsync(c->cand.p, 0, 8, st));
-  CUDA_TRY(cudaEventRecord(c->ev[2], st));
-  if (sample_ids) k_query<false, true><<<(unsigned)grid, 256, 0, st>>>(A);
-  else k_query<false, false><<<(unsigned)grid, 256, 0, st>>>(A);
-  CUDA_TRY(cudaEventRecord(c->ev[3], st));
-  CUDA_TRY(cudaGetLastError());
-
-  // rowptr[0] = 0, rowptr[1..n] = inclusive scan of deg
-  CUDA_TRY(cudaMemsetAsync(c->rowptr.p, 0, 8, st));
-  cub::TransformInputIterator<long long, ToI64, const int32_t*> it(c->deg.as<int32_t>(), ToI64());
-  size_t tb = 0;
-  CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, it, c->rowptr.as<long long>() + 1, (int)n, st));
-  CUDA_TRY(c->temp.ensure(tb));
-  tb = c->temp.bytes;
-  CUDA_TRY(cub::DeviceScan::InclusiveSum(c->temp.p, tb, it, c->rowptr.as<long long>() + 1, (int)n, st));
-  int64_t nnz = 0;
-  unsigned long long cand = 0;
-  CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(&cand, c->cand.p, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  unsigned gq = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>(blocks_for(n, kLightThreads), c->grid_light));
+  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_for(n), c->grid_compact));
+  // staging capacity: candidates of the previous call on this context, else
+  // a generous estimate; an overflow is detected and the pass re-run
+  if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * n, 1 << 20);
+  int64_t H = 0, total_chunks = 0, nnz = 0;
+  unsigned long long ctr[4];
+  int launches = 0;
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CUDA_TRY(c->stage.ensure(4 * (size_t)c->stage_cap));
+    A.stage = c->stage.as<int32_t>();
+    A.stage_cap = c->stage_cap;
+    CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 32, st));
+    CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
+    if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
+    else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
+    launches++;
+    CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    H = (int64_t)(ctr[2] & 0xffffffffull);
+    total_chunks = 0;
+    if (H > 0) {
+      CUDA_TRY(c->nchunks.ensure(4 * (size_t)H));
+      CUDA_TRY(c->chunk_start.ensure(8 * (size_t)(H + 1)));
+      k_heavy_chunks<<<blocks_for(H), 256, 0, st>>>(A.heavy_c, H, c->nchunks.as<int32_t>());
+      hrg_status s = scan_i32_to_i64(c, c->nchunks.as<int32_t>(), c->chunk_start.as<int64_t>(), H);
+      if (s != HRG_OK) return s;
+      CUDA_TRY(cudaMemcpyAsync(&total_chunks, c->chunk_start.as<int64_t>() + H, 8,
+                               cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      CUDA_TRY(c->chunk_hits.ensure(4 * (size_t)total_chunks));
+      A.chunk_start = c->chunk_start.as<int64_t>();
+      A.chunk_hits = c->chunk_hits.as<int32_t>();
+      A.total_chunks = total_chunks;
+      unsigned gh = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
+      if (sample_ids) k_heavy<true><<<gh, 256, 0, st>>>(A, H);
+      else k_heavy<false><<<gh, 256, 0, st>>>(A, H);
+      launches += 2;
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[E_COUNTED], st));
+    CUDA_TRY(cudaGetLastError());
+    hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
+    if (s != HRG_OK) return s;
+    CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if ((ctr[3] & 0xffffffffull) == 0) break;
+    // staging overflowed: size it from the bump allocator's final value
+    c->stage_cap = (int64_t)(ctr[0] + ctr[0] / 8 + 4096);
+    if (attempt == 2) return fail(HRG_ERR_INTERNAL, "staging buffer overflow");
+  }
   if (nnz >= ((int64_t)1 << 31) && sample_ids)
     return fail(HRG_ERR_INTERNAL, "row sort supports at most 2^31-1 CSR entries");
+  // next call: keep ~10% headroom over this call's staging use
+  c->stage_cap = std::max<int64_t>(c->stage_cap, (int64_t)(ctr[0] + ctr[0] / 10 + 4096));
 
   CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
-  A.out = c->idx.as<int32_t>();
-  CUDA_TRY(cudaEventRecord(c->ev[4], st));
-  if (sample_ids) k_query<true, true><<<(unsigned)grid, 256, 0, st>>>(A);
-  else k_query<true, false><<<(unsigned)grid, 256, 0, st>>>(A);
-  CUDA_TRY(cudaEventRecord(c->ev[5], st));
+  int32_t* idx = c->idx.as<int32_t>();
+  const int64_t* rp = c->rowptr.as<int64_t>();
+  CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
+  if (sample_ids) k_compact_light<true><<<gc, 256, 0, st>>>(A, rp, idx);
+  else k_compact_light<false><<<gc, 256, 0, st>>>(A, rp, idx);
+  launches++;
+  if (total_chunks > 0) {
+    CUDA_TRY(c->chunk_off.ensure(8 * (size_t)(total_chunks + 1)));
+    hrg_status s = scan_i32_to_i64(c, c->chunk_hits.as<int32_t>(), c->chunk_off.as<int64_t>(),
+                                   total_chunks);
+    if (s != HRG_OK) return s;
+    unsigned gh = (unsigned)std::max<int64_t>(
+        1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
+    k_compact_heavy<<<gh, 256, 0, st>>>(A, H, c->chunk_off.as<int64_t>(), rp, idx, sample_ids);
+    launches++;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
   CUDA_TRY(cudaGetLastError());
-  int launches = 2;
-  c->idx_final = c->idx.as<int32_t>();
-  if (sample_ids && nnz > 0) {
-    // rows were written in (band, angle) order of the neighbours; hrgen's
-    // Graph keeps each row sorted by id (graph.py:69-71)
+  c->idx_final = idx;
+  if (sample_ids && H > 0) {
+    // heavy rows arrive in (band, angle) order of their neighbours; sort just
+    // those segments (hrgen's Graph keeps every row sorted by id, graph.py:69-71)
+    CUDA_TRY(c->seg_b.ensure(8 * (size_t)H));
+    CUDA_TRY(c->seg_e.ensure(8 * (size_t)H));
+    k_heavy_segments<<<blocks_for(H), 256, 0, st>>>(A, H, rp, c->seg_b.as<int64_t>(),
+                                                     c->seg_e.as<int64_t>());
     CUDA_TRY(c->idx2.ensure(4 * (size_t)nnz));
     size_t sb = 0;
-    const int64_t* rp = c->rowptr.as<int64_t>();
-    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, c->idx.as<int32_t>(),
-                                                c->idx2.as<int32_t>(), (int)nnz, (int)n, rp,
-                                                rp + 1, st));
+    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, idx, c->idx2.as<int32_t>(),
+                                                (int)nnz, (int)H, c->seg_b.as<int64_t>(),
+                                                c->seg_e.as<int64_t>(), st));
     CUDA_TRY(c->temp.ensure(sb));
     sb = c->temp.bytes;
-    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, c->idx.as<int32_t>(),
-                                                c->idx2.as<int32_t>(), (int)nnz, (int)n, rp,
-                                                rp + 1, st));
-    c->idx_final = c->idx2.as<int32_t>();
-    launches += 1;
+    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, idx, c->idx2.as<int32_t>(),
+                                                (int)nnz, (int)H, c->seg_b.as<int64_t>(),
+                                                c->seg_e.as<int64_t>(), st));
+    // copy the sorted heavy segments back into place
+    k_copy_segments<<<(unsigned)std::min<int64_t>(H, 65535), 256, 0, st>>>(
+        c->idx2.as<int32_t>(), idx, c->seg_b.as<int64_t>(), c->seg_e.as<int64_t>(), H);
+    launches += 2;
   }
+  CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
   c->nnz = nnz;
   if (stats) {
     stats->nnz = nnz;
     stats->m = nnz / 2;
-    stats->candidates = (int64_t)cand;
+    stats->candidates = (int64_t)ctr[1];
+    stats->heavy_queries = H;
+    stats->heavy_chunks = total_chunks;
     stats->kernel_launches += launches;
   }
   return HRG_OK;
@@ -287,7 +375,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     stats->alpha = M->alpha;
     stats->n_bands = L;
   }
-  CUDA_TRY(cudaEventRecord(c->ev[0], st));
+  CUDA_TRY(cudaEventRecord(c->ev[E_START], st));
   if (!from_coords) {
     SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
     k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
@@ -304,10 +392,10 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     if (bad) return fail(HRG_ERR_OUT_OF_BOUNDS, "point outside the tree region");
   }
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(c->ev[1], st));
+  CUDA_TRY(cudaEventRecord(c->ev[E_SAMPLED], st));
   hrg_status s = build_index(c, M, S, L, shard, C);
   if (s != HRG_OK) return s;
-  if (stats) stats->kernel_launches = 8;  // sample/keys, sort, gather, 5 index kernels
+  if (stats) stats->kernel_launches = 7;  // sample/keys, gather, 5 index kernels (+ CUB sort)
   s = emit_edges(c, M, L, C, sample_ids, stats);
   if (s != HRG_OK) return s;
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -315,11 +403,14 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   c->have_result = true;
   c->coords_sorted = !sample_ids;
   if (stats) {
-    stats->t_sample_ms = ev_ms(c->ev[0], c->ev[1]);
-    stats->t_build_ms = ev_ms(c->ev[1], c->ev[2]);
-    stats->t_edges_ms = ev_ms(c->ev[2], c->ev[5]);
-    stats->t_query_count_ms = ev_ms(c->ev[2], c->ev[3]);
-    stats->t_query_write_ms = ev_ms(c->ev[4], c->ev[5]);
+    stats->t_sample_ms = ev_ms(c->ev[E_START], c->ev[E_SAMPLED]);
+    stats->t_build_ms = ev_ms(c->ev[E_SAMPLED], c->ev[E_INDEXED]);
+    stats->t_edges_ms = ev_ms(c->ev[E_INDEXED], c->ev[E_ROWSORTED]);
+    stats->t_sort_ms = ev_ms(c->ev[E_SAMPLED], c->ev[E_SORTED]);
+    stats->t_light_ms = ev_ms(c->ev[E_INDEXED], c->ev[E_PLANNED]);
+    stats->t_heavy_ms = ev_ms(c->ev[E_PLANNED], c->ev[E_COUNTED]);
+    stats->t_compact_ms = ev_ms(c->ev[E_WRITE0], c->ev[E_WRITTEN]);
+    stats->t_rowsort_ms = ev_ms(c->ev[E_WRITTEN], c->ev[E_ROWSORTED]);
   }
   return HRG_OK;
 }
@@ -351,8 +442,10 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->s_phi, &c->s_px, &c->s_py, &c->s_cx, &c->s_cy, &c->s_rsq, &c->s_rf,
-                 &c->s_bf, &c->s_rp, &c->s_rn, &c->bands, &c->dir, &c->dir_total, &c->bad,
+                 &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
+                 &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
+                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->seg_b,
+                 &c->seg_e, &c->bands, &c->dir, &c->dir_total, &c->bad,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);

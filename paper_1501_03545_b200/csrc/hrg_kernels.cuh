@@ -4,18 +4,20 @@
 //   k_sample        Philox4x32-10 -> (phi, r_native, r_poincare) per vertex, plus a
 //                   59-bit sort key (radial band << 53 | angular fixed point q).
 //   cub radix sort  keys -> permutation into (band, angle) order.
-//   k_gather        SoA fp64 point/circle records in sorted order: p_x, p_y (the
-//                   point), c_x, c_y, rad^2 (its query circle), correctly rounded
-//                   sin/cos, hrgen's circle transform (geometry.py:141-157).
+//   k_gather        48-byte fp64 candidate records in sorted order: p_x, p_y (the
+//                   point), c_x, c_y, rad^2 (its query circle), id; correctly
+//                   rounded sin/cos, hrgen's circle transform (geometry.py:141-157).
 //   k_band_setup / k_band_minmax / k_dir_fill / k_dir_tail
 //                   per band: position range, min hyperbolic radius, max Poincare
 //                   radius, and an angular directory (bucket -> first position).
-//   k_query<COUNT>  one warp per query vertex: lane j computes the angular window of
-//                   band j, the warp flattens the <=2 position segments per band,
-//                   tests 32 candidates per step with the reference predicate and
-//                   counts hits.
-//   cub scan        degrees -> CSR row pointers.
-//   k_query<WRITE>  same traversal, ballot-compacted ordered writes into the CSR.
+//   k_plan          per query: angular window of every band -> candidate count;
+//                   queries above kLightMax candidates are split into kChunk chunks.
+//   k_light<COUNT>  one thread per light query: bands in order, candidates in
+//                   position order, reference predicate, count hits.
+//   k_heavy<COUNT>  one warp per heavy chunk (hubs): lane j owns band j's window,
+//                   the warp walks the flattened segments 32 candidates at a time.
+//   cub scan        degrees -> CSR row pointers (+ per-chunk offsets of hubs).
+//   k_light/k_heavy<WRITE>  same traversals, writing the rows in order.
 //
 // Replaces hrgen quadtree.py (build 303-340, pack 399-495, query_many 499-631)
 // and generator.py:190-225.
@@ -110,9 +112,19 @@ __global__ void __launch_bounds__(256) k_keys_from_coords(int64_t n, const doubl
   vals[i] = (int32_t)i;
 }
 
-struct SoA {
-  double *phi, *px, *py, *cx, *cy, *rsq;
-  float *rf, *bf;
+// Candidate record: everything one pair test needs about a vertex w, in one
+// 48-byte line fragment: its point (p_x, p_y) for pred(v -> w), its circle
+// (c_x, c_y, rad^2) for pred(w -> v), and its vertex id.
+struct __align__(16) Rec {
+  double px, py, cx, cy, rsq;
+  int32_t id;
+  float pad;
+};
+
+struct QRec {          // query-side extras, per sorted position
+  double* phi;
+  float* rf;           // hyperbolic radius 2*atanh(r) (rounded down)
+  float* bf;           // (1-r)(1+r) (rounded down)
 };
 
 // Gather into (band, angle) order and precompute every per-point quantity the
@@ -121,7 +133,8 @@ struct SoA {
 __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __restrict__ perm,
                                                 const double* __restrict__ phi,
                                                 const double* __restrict__ rp,
-                                                const double* __restrict__ rn, double a, SoA s,
+                                                const double* __restrict__ rn, double a,
+                                                Rec* __restrict__ rec, QRec q,
                                                 double* __restrict__ s_rp,
                                                 double* __restrict__ s_rn) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -132,18 +145,22 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __rest
   sincos_cr(ph, &sn, &cs);
   double cr, rad;
   circle_params(r, a, &cr, &rad);
-  s.phi[p] = ph;
-  s.px[p] = __dmul_rn(r, cs);
-  s.py[p] = __dmul_rn(r, sn);
-  s.cx[p] = __dmul_rn(cr, cs);
-  s.cy[p] = __dmul_rn(cr, sn);
-  s.rsq[p] = __dmul_rn(rad, rad);
+  Rec R;
+  R.px = __dmul_rn(r, cs);
+  R.py = __dmul_rn(r, sn);
+  R.cx = __dmul_rn(cr, cs);
+  R.cy = __dmul_rn(cr, sn);
+  R.rsq = __dmul_rn(rad, rad);
+  R.id = i;
+  R.pad = 0.f;
+  rec[p] = R;
+  q.phi[p] = ph;
   // hyperbolic radius of the stored Poincare point and (1-r)(1+r), both
   // rounded down: only used to size conservative angular windows.
   double one_m = 1.0 - r;
   double re = log1p(2.0 * r / one_m);  // 2*atanh(r)
-  s.rf[p] = __double2float_rd(re);
-  s.bf[p] = __double2float_rd(one_m * (1.0 + r));
+  q.rf[p] = __double2float_rd(re);
+  q.bf[p] = __double2float_rd(one_m * (1.0 + r));
   if (s_rp) s_rp[p] = r;
   if (s_rn) s_rn[p] = rn[i];
 }
@@ -244,106 +261,296 @@ __global__ void k_dir_tail(const uint64_t* __restrict__ keys, const Band* __rest
     dir[B.dir_base + k] = B.end;
 }
 
+constexpr int kLightMax = 256;     // queries with more candidates take the heavy path
+constexpr int kSegCap = 24;        // non-empty band segments a light query may hold
+constexpr int kChunk = 2048;       // heavy-path work item: candidates of one query
+
 struct QueryArgs {
-  SoA s;
-  const int32_t* id;       // sorted position -> vertex id (sample order)
+  const Rec* rec;
+  QRec q;
   const Band* bands;
   const int32_t* dir;
+  const uint64_t* keys;      // sorted (band << 53 | angular key)
   int L;
-  double C;                // 2^53 / (2 pi)
-  float R_pad;             // R rounded up + fp32 slack
-  float a_f;               // cosh R - 1
-  float E_over_tanh;       // fp64 decision-noise constant / tanh(R)
-  int32_t* deg;            // COUNT: row length per vertex id
-  const int64_t* rowptr;   // WRITE: row offsets per vertex id
-  int32_t* out;            // WRITE: CSR indices
-  unsigned long long* cand;  // COUNT: pair tests (stats)
+  double C;                  // 2^53 / (2 pi)
+  float R_pad;               // R rounded up + fp32 slack
+  float a_f;                 // cosh R - 1
+  float E_over_tanh;         // fp64 decision-noise constant / tanh(R)
+  // staging: every query's hits land in a private slice sized by its candidates
+  int32_t* stage;
+  int64_t stage_cap;
+  unsigned long long* bump;  // staging allocator
+  int64_t* stage_off;        // per sorted position
+  int* overflow;
+  // heavy queries (hubs), deferred by the light pass
+  int32_t* heavy_v;          // entry -> sorted position
+  int32_t* heavy_c;          // entry -> candidates
+  unsigned* heavy_n;
+  int32_t* heavy_of;         // sorted position -> entry, or -1
+  const int64_t* chunk_start;// entry -> first chunk (exclusive scan, H + 1)
+  int64_t total_chunks;
+  int32_t* chunk_hits;
+  int32_t* deg;              // row length per vertex id
+  unsigned long long* cand_total;
 };
 
-__device__ __forceinline__ int32_t dir_lookup(const int32_t* dir, int64_t base, int shift,
-                                              double x, double C, int hi) {
-  uint64_t q = qkey(x, C);
-  return __ldg(dir + base + (int64_t)(q >> shift) + hi);
+struct QView {
+  double phi;
+  float rv, bv, sinh_rv;
+};
+
+// drop leading positions whose angular key is below ql / trailing ones above qh
+__device__ __forceinline__ void trim_lo(const uint64_t* keys, int32_t& s, int32_t e, uint64_t ql) {
+  while (s < e && (__ldg(keys + s) & kQMask) < ql) ++s;
+}
+__device__ __forceinline__ void trim_hi(const uint64_t* keys, int32_t s, int32_t& e, uint64_t qh) {
+  while (e > s && (__ldg(keys + e - 1) & kQMask) > qh) --e;
 }
 
-// One warp per query vertex v.
-//  Lane j (< L) sizes band j's angular window for v: every w in the band with
-//  hyperbolic distance below R + eta lies within it, eta bounding the fp64
-//  decision noise of the reference predicate for this (v, band) pair, so no
-//  pair that either orientation of the predicate accepts can fall outside.
-//  The warp then walks the concatenated candidate segments 32 at a time.
-//  Edge {v,w} is decided by the circle of the smaller vertex id, exactly as
-//  hrgen (generator.py:182-187) queries from v and keeps ids > v.
-template <bool kWrite, bool kSampleIds>
-__global__ void __launch_bounds__(256) k_query(QueryArgs A) {
+// Angular window of band B for query q, as <= 2 sorted-position segments
+// [sA, eA) then [sB, eB).  Every w of the band whose hyperbolic distance to q
+// is below R + eta lies inside, where eta bounds the fp64 decision noise of
+// the reference predicate for this (q, band) pair in either orientation
+// (DESIGN.md "window padding"), so no pair the predicate accepts is missed.
+__device__ __forceinline__ void band_window(const QueryArgs& A, const Band& B, const QView& q,
+                                            int32_t& sA, int32_t& eA, int32_t& sB,
+                                            int32_t& eB) {
+  sA = eA = sB = eB = 0;
+  if (B.end <= B.start) return;
+  float bmn = fminf(q.bv, B.bmin);
+  float eta = A.E_over_tanh * (1.0f / bmn + 2.0f / (A.a_f * q.bv * B.bmin));
+  float Rp = A.R_pad + fminf(eta, 64.0f);
+  bool whole = q.rv + B.rmin <= Rp;
+  double dlt = 0.0;
+  if (!whole) {
+    float chR = coshf(Rp);
+    float num = (chR - coshf(q.rv - B.rmin)) + chR * 2e-6f;
+    float s2 = num / (2.0f * q.sinh_rv * B.sinh_rmin);
+    if (!(s2 < 1.0f)) {
+      whole = true;
+    } else {
+      dlt = (double)(2.0f * asinf(sqrtf(fmaxf(s2, 0.0f)))) * (1.0 + 4e-3) + 1e-14;
+      if (dlt >= 3.141592653589793) whole = true;
+    }
+  }
+  if (whole) { sA = B.start; eA = B.end; return; }
+  double lo = q.phi - dlt, hi = q.phi + dlt;
+  const int32_t* d = A.dir + B.dir_base;
+  // the directory resolves a window to whole buckets; the sorted angular keys
+  // then trim the two boundary buckets exactly (keys are monotone in phi)
+  if (lo < 0.0) {
+    const uint64_t qh = qkey(hi, A.C), ql = qkey(lo + kTwoPi, A.C);
+    sA = B.start; eA = __ldg(d + (qh >> B.shift) + 1);
+    sB = __ldg(d + (ql >> B.shift)); eB = B.end;
+    trim_hi(A.keys, sA, eA, qh);
+    trim_lo(A.keys, sB, eB, ql);
+  } else if (hi >= kTwoPi) {
+    const uint64_t qh = qkey(hi - kTwoPi, A.C), ql = qkey(lo, A.C);
+    sA = B.start; eA = __ldg(d + (qh >> B.shift) + 1);
+    sB = __ldg(d + (ql >> B.shift)); eB = B.end;
+    trim_hi(A.keys, sA, eA, qh);
+    trim_lo(A.keys, sB, eB, ql);
+  } else {
+    const uint64_t ql = qkey(lo, A.C), qh = qkey(hi, A.C);
+    sA = __ldg(d + (ql >> B.shift));
+    eA = __ldg(d + (qh >> B.shift) + 1);
+    trim_lo(A.keys, sA, eA, ql);
+    trim_hi(A.keys, sA, eA, qh);
+  }
+  if (sB < eB && sB < eA) { sA = B.start; eA = B.end; sB = eB = 0; }
+}
+
+__device__ __forceinline__ Rec load_rec(const Rec* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  Rec r;
+  r.px = a.x; r.py = a.y; r.cx = b.x; r.cy = b.y; r.rsq = c.x;
+  r.id = (int32_t)(__double_as_longlong(c.y) & 0xffffffffll);
+  r.pad = 0.f;
+  return r;
+}
+
+struct QFull {
+  QView v;
+  double px, py, cx, cy, rsq;
+  int32_t pos, idv;
+};
+
+template <bool kSampleIds>
+__device__ __forceinline__ QFull load_query(const QueryArgs& A, int32_t v) {
+  QFull f;
+  Rec r = load_rec(A.rec + v);
+  f.px = r.px; f.py = r.py; f.cx = r.cx; f.cy = r.cy; f.rsq = r.rsq;
+  f.pos = v;
+  f.idv = kSampleIds ? r.id : v;
+  f.v.phi = A.q.phi[v];
+  f.v.rv = A.q.rf[v];
+  f.v.bv = A.q.bf[v];
+  f.v.sinh_rv = sinhf(f.v.rv);
+  return f;
+}
+
+// Edge {v, w} is decided by the circle of the smaller vertex id, exactly as
+// hrgen queries from v and keeps ids > v (generator.py:182-187).
+template <bool kSampleIds>
+__device__ __forceinline__ bool pair_test(const QFull& f, const Rec& r, int32_t w, int32_t* idw) {
+  int32_t id = kSampleIds ? r.id : w;
+  *idw = id;
+  if (w == f.pos) return false;
+  if (id < f.idv) return ref_pred(f.px, f.py, r.cx, r.cy, r.rsq);  // pred(w -> v)
+  return ref_pred(r.px, r.py, f.cx, f.cy, f.rsq);                  // pred(v -> w)
+}
+
+// Shard query enumeration: flat index t over the bands' [qstart, qend).
+struct QMap {
+  int64_t off[kMaxBands + 1];
+  int32_t qs[kMaxBands];
+};
+
+__device__ __forceinline__ void load_qmap(const QueryArgs& A, QMap& m, Band* sb) {
+  if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int j = 0; j < A.L; ++j) {
+      m.off[j] = acc;
+      m.qs[j] = sb[j].qstart;
+      acc += sb[j].qend - sb[j].qstart;
+    }
+    m.off[A.L] = acc;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int32_t qmap_pos(const QMap& m, int L, int64_t t) {
+  int lo = 0, hi = L;  // largest j with off[j] <= t
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (m.off[mid] <= t) lo = mid; else hi = mid;
+  }
+  return m.qs[lo] + (int32_t)(t - m.off[lo]);
+}
+
+// Light pass: one thread per query.  Windows of all bands first (non-empty
+// segments go to a per-thread list in shared memory), then one flat loop
+// over the query's candidates in (band, angle) order; hits go to the
+// query's staging slice.  Queries with more than kLightMax candidates or
+// kSegCap segments are deferred to the heavy pass.
+constexpr int kLightThreads = 128;
+
+template <bool kSampleIds>
+__global__ void __launch_bounds__(kLightThreads) k_light(QueryArgs A) {
+  __shared__ Band sb[kMaxBands];
+  __shared__ QMap qm;
+  __shared__ int2 segs[kSegCap][kLightThreads];
+  load_qmap(A, qm, sb);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const int64_t total_q = qm.off[A.L];
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cand_local = 0;
+  for (int64_t tile = wid * 32; tile < total_q; tile += nw * 32) {
+    const int64_t t = tile + lane;
+    const bool active = t < total_q;
+    const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
+    QFull f = load_query<kSampleIds>(A, v);
+    int nseg = 0;
+    int32_t c = 0;
+    bool ovf = false;
+    if (active) {
+      for (int j = 0; j < A.L; ++j) {
+        int32_t sA, eA, sB, eB;
+        band_window(A, sb[j], f.v, sA, eA, sB, eB);
+        if (eA > sA) {
+          if (nseg < kSegCap) segs[nseg++][tid] = make_int2(sA, eA - sA); else ovf = true;
+          c += eA - sA;
+        }
+        if (eB > sB) {
+          if (nseg < kSegCap) segs[nseg++][tid] = make_int2(sB, eB - sB); else ovf = true;
+          c += eB - sB;
+        }
+      }
+    }
+    cand_local += (unsigned long long)c;
+    const bool heavy = active && (c > kLightMax || ovf);
+    // staging slices: warp-aggregated allocation for light queries
+    int32_t want = (active && !heavy) ? c : 0;
+    int32_t incl = want;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned long long base = 0;
+    if (lane == 31 && incl > 0) base = atomicAdd(A.bump, (unsigned long long)incl);
+    base = __shfl_sync(FULL, base, 31);
+    if (!active) continue;
+    if (heavy) {
+      unsigned long long hoff = atomicAdd(A.bump, (unsigned long long)c);
+      unsigned e = atomicAdd(A.heavy_n, 1u);
+      A.heavy_v[e] = v;
+      A.heavy_c[e] = c;
+      A.heavy_of[v] = (int32_t)e;
+      A.stage_off[v] = (int64_t)hoff;
+      continue;
+    }
+    const int64_t off = (int64_t)base + incl - want;
+    A.heavy_of[v] = -1;
+    A.stage_off[v] = off;
+    if (off + c > A.stage_cap) { atomicOr(A.overflow, 1); A.deg[f.idv] = 0; continue; }
+    int32_t* out = A.stage + off;
+    int32_t hits = 0;
+    int k = 0;
+    int2 sg = make_int2(0, 0);
+    if (nseg > 0) sg = segs[0][tid];
+    for (int32_t i = 0; i < c; ++i) {
+      while (sg.y == 0) sg = segs[++k][tid];
+      const int32_t w = sg.x;
+      sg.x++; sg.y--;
+      int32_t idw;
+      if (pair_test<kSampleIds>(f, load_rec(A.rec + w), w, &idw)) out[hits++] = idw;
+    }
+    A.deg[f.idv] = hits;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cand_local += __shfl_xor_sync(FULL, cand_local, o);
+  if (lane == 0 && cand_local) atomicAdd(A.cand_total, cand_local);
+}
+
+__global__ void k_heavy_chunks(const int32_t* __restrict__ heavy_c, int64_t H,
+                               int32_t* __restrict__ nchunks) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < H) nchunks[e] = (heavy_c[e] + kChunk - 1) / kChunk;
+}
+
+// Heavy pass: one warp per chunk of kChunk candidates of one deferred query;
+// lanes own bands for the window phase, then stride the chunk 32 candidates
+// at a time (4 batches in flight) with ballot-ordered writes into the
+// chunk's slot of the query's staging slice.
+template <bool kSampleIds>
+__global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
+  __shared__ Band sb[kMaxBands];
+  if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const unsigned FULL = 0xffffffffu;
-
-  // per-lane band constants, resident for the whole kernel
-  Band B;
-  int64_t qoff_lane = INT64_MAX;
-  int64_t total_q = 0;   // queries of this shard = sum of the bands' query ranges
-  for (int j = 0; j < A.L; ++j) {
-    Band t = A.bands[j];
-    if (j == lane) { B = t; qoff_lane = total_q; }
-    total_q += t.qend - t.qstart;
-  }
-  if (lane >= A.L) { B = A.bands[0]; B.start = B.end = 0; }
-  unsigned long long cand_local = 0;
-
-  for (int64_t t = warp; t < total_q; t += nwarps) {
-    unsigned below = __ballot_sync(FULL, qoff_lane <= t);
-    int jq = 31 - __clz(below);
-    int64_t q0 = __shfl_sync(FULL, qoff_lane, jq);
-    int32_t qs = __shfl_sync(FULL, B.qstart, jq);
-    int32_t v = qs + (int32_t)(t - q0);
-
-    const double phi_v = A.s.phi[v];
-    const double px_v = A.s.px[v], py_v = A.s.py[v];
-    const double cx_v = A.s.cx[v], cy_v = A.s.cy[v], rsq_v = A.s.rsq[v];
-    const float rv = A.s.rf[v], bv = A.s.bf[v];
-    const int32_t idv = kSampleIds ? A.id[v] : v;
-
-    // ---- band windows (lane j <-> band j)
-    int32_t sA = 0, eA = 0, sB = 0, eB = 0;
-    if (lane < A.L && B.end > B.start) {
-      float bmn = fminf(bv, B.bmin);
-      float eta = A.E_over_tanh * (1.0f / bmn + 2.0f / (A.a_f * bv * B.bmin));
-      float Rp = A.R_pad + fminf(eta, 64.0f);
-      bool whole = rv + B.rmin <= Rp;
-      double dlt = 0.0;
-      if (!whole) {
-        float chR = coshf(Rp);
-        float num = (chR - coshf(rv - B.rmin)) + chR * 2e-6f;
-        float s2 = num / (2.0f * sinhf(rv) * B.sinh_rmin);
-        if (!(s2 < 1.0f)) {
-          whole = true;
-        } else {
-          dlt = (double)(2.0f * asinf(sqrtf(fmaxf(s2, 0.0f)))) * (1.0 + 4e-3) + 1e-14;
-          if (dlt >= 3.141592653589793) whole = true;
-        }
-      }
-      if (whole) {
-        sA = B.start; eA = B.end;
-      } else {
-        double lo = phi_v - dlt, hi = phi_v + dlt;
-        if (lo < 0.0) {
-          sA = B.start; eA = dir_lookup(A.dir, B.dir_base, B.shift, hi, A.C, 1);
-          sB = dir_lookup(A.dir, B.dir_base, B.shift, lo + kTwoPi, A.C, 0); eB = B.end;
-        } else if (hi >= kTwoPi) {
-          sA = B.start; eA = dir_lookup(A.dir, B.dir_base, B.shift, hi - kTwoPi, A.C, 1);
-          sB = dir_lookup(A.dir, B.dir_base, B.shift, lo, A.C, 0); eB = B.end;
-        } else {
-          sA = dir_lookup(A.dir, B.dir_base, B.shift, lo, A.C, 0);
-          eA = dir_lookup(A.dir, B.dir_base, B.shift, hi, A.C, 1);
-        }
-        if (sB < eB && sB < eA) { sA = B.start; eA = B.end; sB = eB = 0; }
-      }
+  for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
+    int64_t lo = 0, hi = H;  // entry: largest e with chunk_start[e] <= c
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (A.chunk_start[mid] <= c) lo = mid; else hi = mid;
     }
-    const int32_t lenA = eA - sA;
-    const int32_t cnt = lenA + (eB - sB);
+    const int64_t e = lo;
+    const int32_t v = A.heavy_v[e];
+    const int64_t local = c - A.chunk_start[e];
+    QFull f = load_query<kSampleIds>(A, v);
+    int32_t sA = 0, eA = 0, sB = 0, eB = 0;
+    if (lane < A.L) band_window(A, sb[lane], f.v, sA, eA, sB, eB);
+    const int32_t lenA = eA - sA, cnt = lenA + (eB - sB);
     int32_t incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -352,47 +559,230 @@ __global__ void __launch_bounds__(256) k_query(QueryArgs A) {
     }
     const int32_t total = __shfl_sync(FULL, incl, 31);
     const int32_t excl = incl - cnt;
-    cand_local += (unsigned long long)total;
-
-    int64_t row = 0;
-    if (kWrite) row = A.rowptr[idv];
+    const int32_t beg = (int32_t)(local * kChunk);
+    const int32_t end = min(total, beg + kChunk);
+    const int64_t slot = A.stage_off[v] + local * kChunk;
+    int32_t* out = A.stage + slot;
+    const bool fits = slot + (end - beg) <= A.stage_cap;
     int32_t hits = 0;
-    for (int32_t base = 0; base < total; base += 32) {
-      int32_t i = base + lane;
-      int o = 0;
+    for (int32_t base = beg; base < end; base += 128) {
+      int32_t wv[4];
+      bool ok[4];
+      Rec r[4];
 #pragma unroll
-      for (int s = 16; s > 0; s >>= 1) {
-        int32_t ex = __shfl_sync(FULL, excl, o + s);
-        if (ex <= i) o += s;
-      }
-      int32_t tt = i - __shfl_sync(FULL, excl, o);
-      int32_t la = __shfl_sync(FULL, lenA, o);
-      int32_t sa = __shfl_sync(FULL, sA, o);
-      int32_t sb = __shfl_sync(FULL, sB, o);
-      int32_t w = tt < la ? sa + tt : sb + (tt - la);
-      bool hit = false;
-      int32_t idw = w;
-      if (i < total && w != v) {
-        if (kSampleIds) idw = A.id[w];
-        if (idw < idv) {  // edge decided by w's circle (pred(w -> v))
-          hit = ref_pred(px_v, py_v, A.s.cx[w], A.s.cy[w], A.s.rsq[w]);
-        } else {          // by v's circle (pred(v -> w))
-          hit = ref_pred(A.s.px[w], A.s.py[w], cx_v, cy_v, rsq_v);
+      for (int u = 0; u < 4; ++u) {
+        int32_t i = base + 32 * u + lane;
+        int o = 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+          int32_t ex = __shfl_sync(FULL, excl, o + s);
+          if (ex <= i) o += s;
         }
+        int32_t tt = i - __shfl_sync(FULL, excl, o);
+        int32_t la = __shfl_sync(FULL, lenA, o);
+        int32_t sa = __shfl_sync(FULL, sA, o);
+        int32_t sbb = __shfl_sync(FULL, sB, o);
+        wv[u] = tt < la ? sa + tt : sbb + (tt - la);
+        ok[u] = i < end;
+        if (ok[u]) r[u] = load_rec(A.rec + wv[u]);
       }
-      unsigned bal = __ballot_sync(FULL, hit);
-      if (kWrite && hit) A.out[row + hits + __popc(bal & ((1u << lane) - 1u))] = idw;
-      hits += __popc(bal);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int32_t idw = 0;
+        bool hit = ok[u] && pair_test<kSampleIds>(f, r[u], wv[u], &idw);
+        unsigned bal = __ballot_sync(FULL, hit);
+        if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = idw;
+        hits += __popc(bal);
+      }
     }
-    if (!kWrite && lane == 0) A.deg[idv] = hits;
-  }
-  if (!kWrite && A.cand) {
-    if (lane == 0) atomicAdd(A.cand, cand_local);
+    if (lane == 0) {
+      if (!fits) atomicOr(A.overflow, 1);
+      A.chunk_hits[c] = hits;
+      atomicAdd(&A.deg[f.idv], hits);
+    }
   }
 }
 
-// Sector bookkeeping for sample-order rows of other shards: nothing to do --
-// deg[] is cleared before the count pass, so foreign rows stay empty.
+// Warp-wide bitonic sort of 32*E keys held E per lane (element index
+// e = lane*E + t), ascending.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(int32_t (&x)[E], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int e = lane * E + t;
+          int32_t y = __shfl_xor_sync(0xffffffffu, x[t], lj);
+          const bool up = (e & k) == 0;
+          const bool lower = (e & j) == 0;
+          // keep min if (lower == up) else max
+          x[t] = (lower == up) ? min(x[t], y) : max(x[t], y);
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < E; ++t) {
+          const int t2 = t ^ j;
+          if (t2 > t) {
+            const int e = lane * E + t;
+            const bool up = (e & k) == 0;
+            int32_t a = x[t], b = x[t2];
+            x[t] = up ? min(a, b) : max(a, b);
+            x[t2] = up ? max(a, b) : min(a, b);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void copy_sorted_row(const int32_t* __restrict__ src,
+                                                int32_t* __restrict__ dst, int32_t len,
+                                                int lane) {
+  int32_t x[E];
+#pragma unroll
+  for (int t = 0; t < E; ++t) {
+    const int e = lane * E + t;
+    x[t] = e < len ? __ldg(src + e) : INT32_MAX;
+  }
+  warp_bitonic<E>(x, lane);
+#pragma unroll
+  for (int t = 0; t < E; ++t) {
+    const int e = lane * E + t;
+    if (e < len) dst[e] = x[t];
+  }
+}
+
+// Compaction of light rows: a warp owns 32 consecutive queries and moves
+// their rows, one row at a time 32 lanes wide, from the staging slices to
+// the CSR slots rowptr[id].  With sample-order ids the row is sorted on the
+// way through (registers + shuffles), which is the order hrgen's Graph keeps.
+template <bool kSampleIds>
+__global__ void __launch_bounds__(256) k_compact_light(QueryArgs A,
+                                                       const int64_t* __restrict__ rowptr,
+                                                       int32_t* __restrict__ idx) {
+  __shared__ Band sb[kMaxBands];
+  __shared__ QMap qm;
+  load_qmap(A, qm, sb);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t total_q = qm.off[A.L];
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t tile = wid * 32; tile < total_q; tile += nw * 32) {
+    const int64_t t = tile + lane;
+    const bool active = t < total_q;
+    const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
+    const int32_t idv = kSampleIds ? (int32_t)(__double_as_longlong(__ldg(
+                                         reinterpret_cast<const double*>(A.rec + v) + 5)) &
+                                     0xffffffffll)
+                                   : v;
+    const bool light = active && A.heavy_of[v] < 0;
+    const int64_t dst = light ? rowptr[idv] : 0;
+    const int32_t len = light ? (int32_t)(rowptr[idv + 1] - dst) : 0;
+    const int64_t src = light ? A.stage_off[v] : 0;
+    unsigned todo = __ballot_sync(FULL, len > 0);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t d = __shfl_sync(FULL, dst, l);
+      const int32_t ln = __shfl_sync(FULL, len, l);
+      const int64_t s0 = __shfl_sync(FULL, src, l);
+      const int32_t* in = A.stage + s0;
+      int32_t* out = idx + d;
+      if (!kSampleIds) {
+        int32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = lane + 32 * u;
+          x[u] = k < ln ? __ldg(in + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = lane + 32 * u;
+          if (k < ln) out[k] = x[u];
+        }
+      } else if (ln <= 32) {
+        copy_sorted_row<1>(in, out, ln, lane);
+      } else if (ln <= 64) {
+        copy_sorted_row<2>(in, out, ln, lane);
+      } else if (ln <= 128) {
+        copy_sorted_row<4>(in, out, ln, lane);
+      } else {
+        copy_sorted_row<8>(in, out, ln, lane);
+      }
+    }
+  }
+}
+
+// Compaction of heavy rows: one warp per chunk; the chunk's hits go to
+// rowptr[id] + (hits of the row's earlier chunks).
+__global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
+                                                       const int64_t* __restrict__ chunk_off,
+                                                       const int64_t* __restrict__ rowptr,
+                                                       int32_t* __restrict__ idx,
+                                                       bool sample_ids) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
+    int64_t lo = 0, hi = H;
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (A.chunk_start[mid] <= c) lo = mid; else hi = mid;
+    }
+    const int64_t e = lo;
+    const int32_t v = A.heavy_v[e];
+    const int32_t idv = sample_ids ? (int32_t)(__double_as_longlong(__ldg(
+                                         reinterpret_cast<const double*>(A.rec + v) + 5)) &
+                                     0xffffffffll)
+                                   : v;
+    const int64_t c0 = A.chunk_start[e];
+    const int64_t d = rowptr[idv] + (chunk_off[c] - chunk_off[c0]);
+    const int32_t h = A.chunk_hits[c];
+    const int32_t* in = A.stage + A.stage_off[v] + (c - c0) * kChunk;
+    for (int32_t k0 = 0; k0 < h; k0 += 256) {
+      int32_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + lane + 32 * u;
+        x[u] = k < h ? __ldg(in + k) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + lane + 32 * u;
+        if (k < h) idx[d + k] = x[u];
+      }
+    }
+  }
+}
+
+// begin/end offsets of the heavy rows (sample-order ids: these rows still
+// need sorting after the chunk-parallel copy)
+__global__ void k_heavy_segments(QueryArgs A, int64_t H, const int64_t* __restrict__ rowptr,
+                                 int64_t* __restrict__ seg_begin, int64_t* __restrict__ seg_end) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= H) return;
+  const int32_t v = A.heavy_v[e];
+  const int32_t idv = (int32_t)(__double_as_longlong(
+                                    __ldg(reinterpret_cast<const double*>(A.rec + v) + 5)) &
+                                0xffffffffll);
+  seg_begin[e] = rowptr[idv];
+  seg_end[e] = rowptr[idv + 1];
+}
+
+__global__ void __launch_bounds__(256) k_copy_segments(const int32_t* __restrict__ from,
+                                                       int32_t* __restrict__ to,
+                                                       const int64_t* __restrict__ b,
+                                                       const int64_t* __restrict__ e,
+                                                       int64_t H) {
+  for (int64_t s = blockIdx.x; s < H; s += gridDim.x)
+    for (int64_t k = b[s] + threadIdx.x; k < e[s]; k += blockDim.x) to[k] = from[k];
+}
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,
                                                 double* __restrict__ s, double* __restrict__ c) {

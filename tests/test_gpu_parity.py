@@ -272,7 +272,7 @@ def test_random_coordinates_many_radii(oracle):
 def test_out_of_bounds_coordinates_raise():
     R = 10.0
     with pytest.raises(P.OutOfBoundsError):
-        P.edges_from_coordinates(VertexCoordinates(np.array([0.0]), None, np.array([0.9999])), R)
+        P.edges_from_coordinates(VertexCoordinates(np.array([0.0]), None, np.array([0.99995])), R)
     with pytest.raises(P.OutOfBoundsError):
         P.edges_from_coordinates(VertexCoordinates(np.array([-0.1]), None, np.array([0.5])), R)
     with pytest.raises(P.OutOfBoundsError):
