@@ -76,7 +76,7 @@ struct hrg_context {
   Buf rec, s_phi, s_rf, s_bf, s_rp, s_rn;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
-      chunk_off, seg_b, seg_e;
+      chunk_off, huge_b, huge_e, slots, wtab, job_src, job_dst, job_ns, job_len, job_big;
   int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad;
@@ -130,7 +130,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
   CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(64));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
-  CUDA_TRY(c->heavy_of.ensure(i32));
+  CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
   CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
   CUDA_TRY(c->dir.ensure(4 * (size_t)(2 * n + 2 * kMaxBands + 64)));
@@ -178,7 +178,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   }
   k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>());
-  k_band_minmax<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(),
+  k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(),
                                                c->s_bf.as<float>(), c->bands.as<Band>());
   k_band_finish<<<1, 64, 0, st>>>(c->bands.as<Band>(), L);
   k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
@@ -225,48 +225,56 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   A.keys = c->keys_out.as<uint64_t>();
   A.L = L;
   A.C = C;
-  A.R_pad = nextafterf((float)M->R, INFINITY) + 3e-5f;
-  A.a_f = (float)M->cosh_r_minus_1;
-  // 2^-45 bounds the absolute fp64 error of dx*dx+dy*dy and rad^2 (all
-  // operands <= 1 in magnitude); see DESIGN.md "window padding".
-  A.E_over_tanh = (float)(std::ldexp(1.0, -45) / std::tanh(M->R)) * 1.001f;
   A.bump = c->counters.as<unsigned long long>();
   A.cand_total = c->counters.as<unsigned long long>() + 1;
   A.heavy_n = reinterpret_cast<unsigned*>(c->counters.as<unsigned long long>() + 2);
   A.overflow = reinterpret_cast<int*>(c->counters.as<unsigned long long>() + 3);
   A.stage_off = c->stage_off.as<int64_t>();
+  A.slots = c->slots.as<int32_t>();
   A.heavy_v = c->heavy_v.as<int32_t>();
   A.heavy_c = c->heavy_c.as<int32_t>();
   A.heavy_of = c->heavy_of.as<int32_t>();
   A.deg = c->deg.as<int32_t>();
 
+  // window table: one row per 1/16 of query radius, one column per band.
+  // 2^-45 bounds the absolute fp64 error of dx*dx+dy*dy and rad^2 (all
+  // operands <= 1 in magnitude); see DESIGN.md "window padding".
+  const int rows = (int)std::ceil(M->R / (double)kRowStep) + 2;
+  CUDA_TRY(c->wtab.ensure(sizeof(float) * (size_t)rows * L));
+  A.wtab = c->wtab.as<float>();
+  A.wrows = rows;
+  const double E_over_tanh = std::ldexp(1.0, -45) / std::tanh(M->R) * 1.001;
+  k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->R, M->cosh_r_minus_1, E_over_tanh,
+                                      c->wtab.as<float>());
+  int launches = 1;
+
   if (c->grid_light == 0) {
     c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
-    c->grid_compact = occupancy_grid(c, k_compact_light<true>);
+    c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
   }
   unsigned gq = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(n, kLightThreads), c->grid_light));
-  unsigned gc = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks_for(n), c->grid_compact));
-  // staging capacity: candidates of the previous call on this context, else
-  // a generous estimate; an overflow is detected and the pass re-run
+  unsigned gc = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>(blocks_for(n, kCompactThreads), c->grid_compact));
+  // staging capacity: the previous call's use on this context, else a
+  // generous estimate; an overflow is detected and the pass re-run
   if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * n, 1 << 20);
   int64_t H = 0, total_chunks = 0, nnz = 0;
-  unsigned long long ctr[4];
-  int launches = 0;
+  unsigned long long ctr[8];
   for (int attempt = 0; attempt < 3; ++attempt) {
     CUDA_TRY(c->stage.ensure(4 * (size_t)c->stage_cap));
     A.stage = c->stage.as<int32_t>();
     A.stage_cap = c->stage_cap;
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
-    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 32, st));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 64, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
     else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
     launches++;
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     H = (int64_t)(ctr[2] & 0xffffffffull);
     total_chunks = 0;
@@ -294,24 +302,44 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
     if (s != HRG_OK) return s;
     CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 32, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if ((ctr[3] & 0xffffffffull) == 0) break;
     // staging overflowed: size it from the bump allocator's final value
     c->stage_cap = (int64_t)(ctr[0] + ctr[0] / 8 + 4096);
     if (attempt == 2) return fail(HRG_ERR_INTERNAL, "staging buffer overflow");
   }
-  if (nnz >= ((int64_t)1 << 31) && sample_ids)
-    return fail(HRG_ERR_INTERNAL, "row sort supports at most 2^31-1 CSR entries");
   // next call: keep ~10% headroom over this call's staging use
   c->stage_cap = std::max<int64_t>(c->stage_cap, (int64_t)(ctr[0] + ctr[0] / 10 + 4096));
 
   CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
   int32_t* idx = c->idx.as<int32_t>();
   const int64_t* rp = c->rowptr.as<int64_t>();
+  // sort jobs: light rows of more than 32 slots and (sample order) heavy rows
+  const int64_t jcap = n + H + 1;
+  CUDA_TRY(c->job_src.ensure(8 * (size_t)jcap));
+  CUDA_TRY(c->job_dst.ensure(8 * (size_t)jcap));
+  CUDA_TRY(c->job_ns.ensure(4 * (size_t)jcap));
+  CUDA_TRY(c->job_len.ensure(4 * (size_t)jcap));
+  CUDA_TRY(c->job_big.ensure(4 * (size_t)jcap));
+  const int64_t huge_cap = nnz / (kBucketMax + 1) + 1;
+  CUDA_TRY(c->huge_b.ensure(8 * (size_t)huge_cap));
+  CUDA_TRY(c->huge_e.ensure(8 * (size_t)huge_cap));
+  unsigned long long* ctrs = c->counters.as<unsigned long long>();
+  SortJobs J;
+  J.src = c->job_src.as<int64_t>();
+  J.dst = c->job_dst.as<int64_t>();
+  J.ns = c->job_ns.as<int32_t>();
+  J.len = c->job_len.as<int32_t>();
+  J.n = reinterpret_cast<unsigned*>(ctrs + 4);
+  J.nbig = reinterpret_cast<unsigned*>(ctrs + 5);
+  J.big = c->job_big.as<int32_t>();
+  J.nhuge = reinterpret_cast<unsigned*>(ctrs + 6);
+  J.huge_b = c->huge_b.as<int64_t>();
+  J.huge_e = c->huge_e.as<int64_t>();
   CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
-  if (sample_ids) k_compact_light<true><<<gc, 256, 0, st>>>(A, rp, idx);
-  else k_compact_light<false><<<gc, 256, 0, st>>>(A, rp, idx);
+  if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
+  else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
   launches++;
   if (total_chunks > 0) {
     CUDA_TRY(c->chunk_off.ensure(8 * (size_t)(total_chunks + 1)));
@@ -322,31 +350,42 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
         1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
     k_compact_heavy<<<gh, 256, 0, st>>>(A, H, c->chunk_off.as<int64_t>(), rp, idx, sample_ids);
     launches++;
+    if (sample_ids) {
+      k_queue_heavy_rows<<<blocks_for(H), 256, 0, st>>>(A, H, rp, J);
+      launches++;
+    }
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
+  if (sample_ids) {
+    k_sort_warp<true><<<8 * c->sm_count, 256, 0, st>>>(c->stage.as<int32_t>(), idx, J);
+    k_sort_block<<<8 * c->sm_count, kBucketThreads, 0, st>>>(c->stage.as<int32_t>(), idx, J, n);
+    launches += 2;
+  } else {
+    k_sort_warp<false><<<8 * c->sm_count, 256, 0, st>>>(c->stage.as<int32_t>(), idx, J);
+    launches += 1;
+  }
   CUDA_TRY(cudaGetLastError());
   c->idx_final = idx;
-  if (sample_ids && H > 0) {
-    // heavy rows arrive in (band, angle) order of their neighbours; sort just
-    // those segments (hrgen's Graph keeps every row sorted by id, graph.py:69-71)
-    CUDA_TRY(c->seg_b.ensure(8 * (size_t)H));
-    CUDA_TRY(c->seg_e.ensure(8 * (size_t)H));
-    k_heavy_segments<<<blocks_for(H), 256, 0, st>>>(A, H, rp, c->seg_b.as<int64_t>(),
-                                                     c->seg_e.as<int64_t>());
-    CUDA_TRY(c->idx2.ensure(4 * (size_t)nnz));
-    size_t sb = 0;
-    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, idx, c->idx2.as<int32_t>(),
-                                                (int)nnz, (int)H, c->seg_b.as<int64_t>(),
-                                                c->seg_e.as<int64_t>(), st));
-    CUDA_TRY(c->temp.ensure(sb));
-    sb = c->temp.bytes;
-    CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, idx, c->idx2.as<int32_t>(),
-                                                (int)nnz, (int)H, c->seg_b.as<int64_t>(),
-                                                c->seg_e.as<int64_t>(), st));
-    // copy the sorted heavy segments back into place
-    k_copy_segments<<<(unsigned)std::min<int64_t>(H, 65535), 256, 0, st>>>(
-        c->idx2.as<int32_t>(), idx, c->seg_b.as<int64_t>(), c->seg_e.as<int64_t>(), H);
-    launches += 2;
+  if (sample_ids) {
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t nh = (int64_t)(ctr[6] & 0xffffffffull);
+    if (nh > 0) {
+      // the few hub rows above kBucketMax: segmented sort, then copy back
+      CUDA_TRY(c->idx2.ensure(4 * (size_t)nnz));
+      size_t sb = 0;
+      CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, idx, c->idx2.as<int32_t>(),
+                                                  (int)nnz, (int)nh, c->huge_b.as<int64_t>(),
+                                                  c->huge_e.as<int64_t>(), st));
+      CUDA_TRY(c->temp.ensure(sb));
+      sb = c->temp.bytes;
+      CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, idx, c->idx2.as<int32_t>(),
+                                                  (int)nnz, (int)nh, c->huge_b.as<int64_t>(),
+                                                  c->huge_e.as<int64_t>(), st));
+      k_copy_segments<<<(unsigned)std::min<int64_t>(nh, 65535), 1024, 0, st>>>(
+          c->idx2.as<int32_t>(), idx, c->huge_b.as<int64_t>(), c->huge_e.as<int64_t>(), nh);
+      launches++;
+    }
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
   c->nnz = nnz;
@@ -444,8 +483,9 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
                  &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
-                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->seg_b,
-                 &c->seg_e, &c->bands, &c->dir, &c->dir_total, &c->bad,
+                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->huge_b,
+                 &c->huge_e, &c->slots, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
+                 &c->job_len, &c->job_big, &c->bands, &c->dir, &c->dir_total, &c->bad,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);

@@ -209,26 +209,32 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
   }
 }
 
-// Per-band min radius / min (1-r)(1+r): warp-aggregated atomicMin on the bit
-// patterns of positive floats (order-preserving, so deterministic).
+// Per-band min radius / min (1-r)(1+r): a block reduces its (few) bands in
+// shared memory, then one atomicMin per band per block on the bit patterns of
+// positive floats (order-preserving, so deterministic).
 __global__ void __launch_bounds__(256) k_band_minmax(int64_t n, const uint64_t* __restrict__ keys,
                                                      const float* __restrict__ rf,
                                                      const float* __restrict__ bf,
                                                      Band* __restrict__ bands) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int lane = threadIdx.x & 31;
-  bool ok = p < n;
-  int band = ok ? (int)(keys[p] >> kQBits) : -1;
-  int r = ok ? __float_as_int(rf[p]) : 0x7f800000;
-  int b = ok ? __float_as_int(bf[p]) : 0x7f800000;
-  // lanes of one band are contiguous (sorted keys): reduce per group, one
-  // atomic per group leader
-  unsigned same = __match_any_sync(0xffffffffu, band);
-  r = (int)__reduce_min_sync(same, (unsigned)r);
-  b = (int)__reduce_min_sync(same, (unsigned)b);
-  if (ok && lane == __ffs(same) - 1) {
-    atomicMin((int*)&bands[band].rmin, r);
-    atomicMin((int*)&bands[band].bmin, b);
+  __shared__ int sr[kMaxBands], sbm[kMaxBands];
+  if (threadIdx.x < kMaxBands) { sr[threadIdx.x] = 0x7f800000; sbm[threadIdx.x] = 0x7f800000; }
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int band = (int)(keys[p] >> kQBits);
+    const int r = __float_as_int(rf[p]), b = __float_as_int(bf[p]);
+    const unsigned same = __match_any_sync(__activemask(), band);
+    const int rm = (int)__reduce_min_sync(same, (unsigned)r);
+    const int bm = (int)__reduce_min_sync(same, (unsigned)b);
+    if ((threadIdx.x & 31) == __ffs(same) - 1) {
+      atomicMin(&sr[band], rm);
+      atomicMin(&sbm[band], bm);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxBands && sr[threadIdx.x] != 0x7f800000) {
+    atomicMin((int*)&bands[threadIdx.x].rmin, sr[threadIdx.x]);
+    atomicMin((int*)&bands[threadIdx.x].bmin, sbm[threadIdx.x]);
   }
 }
 
@@ -261,9 +267,11 @@ __global__ void k_dir_tail(const uint64_t* __restrict__ keys, const Band* __rest
     dir[B.dir_base + k] = B.end;
 }
 
-constexpr int kLightMax = 256;     // queries with more candidates take the heavy path
+constexpr int kLightMax = 2048;    // queries with more candidates take the heavy path
 constexpr int kSegCap = 24;        // non-empty band segments a light query may hold
 constexpr int kChunk = 2048;       // heavy-path work item: candidates of one query
+constexpr int kLightThreads = 128;
+constexpr float kRowStep = 1.0f / 16.0f;  // window table: query-radius row height
 
 struct QueryArgs {
   const Rec* rec;
@@ -271,16 +279,17 @@ struct QueryArgs {
   const Band* bands;
   const int32_t* dir;
   const uint64_t* keys;      // sorted (band << 53 | angular key)
+  const float* wtab;         // window half-width per (query-radius row, band); >= pi: whole band
+  int wrows;
   int L;
   double C;                  // 2^53 / (2 pi)
-  float R_pad;               // R rounded up + fp32 slack
-  float a_f;                 // cosh R - 1
-  float E_over_tanh;         // fp64 decision-noise constant / tanh(R)
-  // staging: every query's hits land in a private slice sized by its candidates
+  // staging: every light query owns one slot per candidate (hit id or -1);
+  // a heavy query's slice holds its chunks' compacted hits at chunk * kChunk
   int32_t* stage;
   int64_t stage_cap;
   unsigned long long* bump;  // staging allocator
   int64_t* stage_off;        // per sorted position
+  int32_t* slots;            // per sorted position: candidates (= slots for light)
   int* overflow;
   // heavy queries (hubs), deferred by the light pass
   int32_t* heavy_v;          // entry -> sorted position
@@ -294,11 +303,6 @@ struct QueryArgs {
   unsigned long long* cand_total;
 };
 
-struct QView {
-  double phi;
-  float rv, bv, sinh_rv;
-};
-
 // drop leading positions whose angular key is below ql / trailing ones above qh
 __device__ __forceinline__ void trim_lo(const uint64_t* keys, int32_t& s, int32_t e, uint64_t ql) {
   while (s < e && (__ldg(keys + s) & kQMask) < ql) ++s;
@@ -307,34 +311,52 @@ __device__ __forceinline__ void trim_hi(const uint64_t* keys, int32_t s, int32_t
   while (e > s && (__ldg(keys + e - 1) & kQMask) > qh) --e;
 }
 
-// Angular window of band B for query q, as <= 2 sorted-position segments
-// [sA, eA) then [sB, eB).  Every w of the band whose hyperbolic distance to q
-// is below R + eta lies inside, where eta bounds the fp64 decision noise of
-// the reference predicate for this (q, band) pair in either orientation
-// (DESIGN.md "window padding"), so no pair the predicate accepts is missed.
-__device__ __forceinline__ void band_window(const QueryArgs& A, const Band& B, const QView& q,
-                                            int32_t& sA, int32_t& eA, int32_t& sB,
-                                            int32_t& eB) {
+// Half-width of the angular window in which band B can hold a vertex within
+// hyperbolic distance R + eta of a query at radius >= rq whose (1-r)(1+r) is
+// >= bq.  eta bounds the fp64 decision noise of the reference predicate for
+// the pair in either orientation, so no pair the
+// predicate accepts falls outside.  Returns >= pi for "the whole band".
+__device__ __forceinline__ double window_halfwidth(double R, double a, double E_over_tanh, double rq,
+                                                   double bq, double rb, double bb) {
+  const double pi = 3.141592653589793;
+  const double eta = E_over_tanh * (1.0 / fmin(bq, bb) + 2.0 / (a * bq * bb)) + 3e-5;
+  const double Rp = R + fmin(eta, 64.0);
+  if (rq + rb <= Rp) return 4.0;
+  // cosh R' = cosh(rq - rb) + 2 sinh rq sinh rb sin^2(d/2) at the widest point
+  const double s2 = (cosh(Rp) - cosh(rq - rb)) / (2.0 * sinh(rq) * sinh(rb));
+  if (!(s2 < 1.0)) return 4.0;
+  const double d = 2.0 * asin(sqrt(fmax(s2, 0.0))) * (1.0 + 1e-6) + 1e-13;
+  return d >= pi ? 4.0 : d;
+}
+
+// Window table: row s covers query radii [s*kRowStep, (s+1)*kRowStep).
+__global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, double R,
+                               double a, double E_over_tanh, float* __restrict__ wtab) {
+  const int s = blockIdx.x, j = threadIdx.x;
+  if (s >= rows || j >= L) return;
+  const Band B = bands[j];
+  float out = 0.0f;
+  if (B.end > B.start) {
+    const double rq = s * (double)kRowStep;
+    // (1-r)(1+r) = 1/cosh^2(r/2) is smallest at the row's top (+ fp32 slack)
+    const double ch = cosh(0.5 * (rq + kRowStep + 1e-5));
+    const double bq = 0.99 / (ch * ch);
+    const double d = window_halfwidth(R, a, E_over_tanh, rq, bq, (double)B.rmin, (double)B.bmin);
+    out = __double2float_ru(d);
+  }
+  wtab[s * L + j] = out;
+}
+
+// Window of band B for a query at angle phi with table half-width dlt, as
+// <= 2 sorted-position segments [sA, eA) then [sB, eB).
+__device__ __forceinline__ void band_segments(const QueryArgs& A, const Band& B, double phi,
+                                              float dlt_f, int32_t& sA, int32_t& eA,
+                                              int32_t& sB, int32_t& eB) {
   sA = eA = sB = eB = 0;
   if (B.end <= B.start) return;
-  float bmn = fminf(q.bv, B.bmin);
-  float eta = A.E_over_tanh * (1.0f / bmn + 2.0f / (A.a_f * q.bv * B.bmin));
-  float Rp = A.R_pad + fminf(eta, 64.0f);
-  bool whole = q.rv + B.rmin <= Rp;
-  double dlt = 0.0;
-  if (!whole) {
-    float chR = coshf(Rp);
-    float num = (chR - coshf(q.rv - B.rmin)) + chR * 2e-6f;
-    float s2 = num / (2.0f * q.sinh_rv * B.sinh_rmin);
-    if (!(s2 < 1.0f)) {
-      whole = true;
-    } else {
-      dlt = (double)(2.0f * asinf(sqrtf(fmaxf(s2, 0.0f)))) * (1.0 + 4e-3) + 1e-14;
-      if (dlt >= 3.141592653589793) whole = true;
-    }
-  }
-  if (whole) { sA = B.start; eA = B.end; return; }
-  double lo = q.phi - dlt, hi = q.phi + dlt;
+  if (dlt_f >= 3.14159265f) { sA = B.start; eA = B.end; return; }
+  const double dlt = (double)dlt_f;
+  const double lo = phi - dlt, hi = phi + dlt;
   const int32_t* d = A.dir + B.dir_base;
   // the directory resolves a window to whole buckets; the sorted angular keys
   // then trim the two boundary buckets exactly (keys are monotone in phi)
@@ -360,6 +382,12 @@ __device__ __forceinline__ void band_window(const QueryArgs& A, const Band& B, c
   if (sB < eB && sB < eA) { sA = B.start; eA = B.end; sB = eB = 0; }
 }
 
+__device__ __forceinline__ const float* wtab_row(const QueryArgs& A, float rv) {
+  int row = (int)(rv * (1.0f / kRowStep));
+  row = min(max(row, 0), A.wrows - 1);
+  return A.wtab + row * A.L;
+}
+
 __device__ __forceinline__ Rec load_rec(const Rec* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
   double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
@@ -370,8 +398,12 @@ __device__ __forceinline__ Rec load_rec(const Rec* p) {
   return r;
 }
 
+__device__ __forceinline__ int32_t rec_id(const Rec* p) {
+  return (int32_t)(__double_as_longlong(__ldg(reinterpret_cast<const double*>(p) + 5)) &
+                   0xffffffffll);
+}
+
 struct QFull {
-  QView v;
   double px, py, cx, cy, rsq;
   int32_t pos, idv;
 };
@@ -383,10 +415,6 @@ __device__ __forceinline__ QFull load_query(const QueryArgs& A, int32_t v) {
   f.px = r.px; f.py = r.py; f.cx = r.cx; f.cy = r.cy; f.rsq = r.rsq;
   f.pos = v;
   f.idv = kSampleIds ? r.id : v;
-  f.v.phi = A.q.phi[v];
-  f.v.rv = A.q.rf[v];
-  f.v.bv = A.q.bf[v];
-  f.v.sinh_rv = sinhf(f.v.rv);
   return f;
 }
 
@@ -431,22 +459,71 @@ __device__ __forceinline__ int32_t qmap_pos(const QMap& m, int L, int64_t t) {
   return m.qs[lo] + (int32_t)(t - m.off[lo]);
 }
 
-// Light pass: one thread per query.  Windows of all bands first (non-empty
-// segments go to a per-thread list in shared memory), then one flat loop
-// over the query's candidates in (band, angle) order; hits go to the
-// query's staging slice.  Queries with more than kLightMax candidates or
-// kSegCap segments are deferred to the heavy pass.
-constexpr int kLightThreads = 128;
+// Raw (directory-resolved) window of band B: segments [sA,eA) and [sB,eB)
+// cover whole buckets; tlA/thA/tlB are the angular keys the exact trim
+// enforces (0 / kQMask+1 = no trim on that side).
+struct RawWin {
+  int32_t sA, eA, sB, eB;
+  uint64_t tlA, thA, tlB;
+};
 
+__device__ __forceinline__ RawWin raw_window(const QueryArgs& A, const Band& B, double phi,
+                                             float dlt_f) {
+  RawWin r;
+  r.sA = r.eA = r.sB = r.eB = 0;
+  r.tlA = 0; r.thA = kQMask + 1; r.tlB = 0;
+  if (B.end <= B.start) return r;
+  if (dlt_f >= 3.14159265f) { r.sA = B.start; r.eA = B.end; return r; }
+  const double dlt = (double)dlt_f;
+  const double lo = phi - dlt, hi = phi + dlt;
+  const int32_t* d = A.dir + B.dir_base;
+  if (lo < 0.0 || hi >= kTwoPi) {
+    const uint64_t qh = qkey(lo < 0.0 ? hi : hi - kTwoPi, A.C);
+    const uint64_t ql = qkey(lo < 0.0 ? lo + kTwoPi : lo, A.C);
+    r.sA = B.start; r.eA = __ldg(d + (qh >> B.shift) + 1); r.thA = qh;
+    r.sB = __ldg(d + (ql >> B.shift)); r.eB = B.end; r.tlB = ql;
+  } else {
+    const uint64_t ql = qkey(lo, A.C), qh = qkey(hi, A.C);
+    r.sA = __ldg(d + (ql >> B.shift)); r.eA = __ldg(d + (qh >> B.shift) + 1);
+    r.tlA = ql; r.thA = qh;
+  }
+  return r;
+}
+
+// One trim step with the boundary keys already loaded, then finish (rare:
+// two or more out-of-window points in one boundary bucket) with a loop.
+__device__ __forceinline__ void finish_trim(const uint64_t* keys, RawWin& r, uint64_t kA0,
+                                            uint64_t kA1, uint64_t kB0) {
+  if (r.sA < r.eA && (kA0 & kQMask) < r.tlA) { ++r.sA; trim_lo(keys, r.sA, r.eA, r.tlA); }
+  if (r.sA < r.eA && (kA1 & kQMask) > r.thA) { --r.eA; trim_hi(keys, r.sA, r.eA, r.thA); }
+  if (r.sB < r.eB && (kB0 & kQMask) < r.tlB) { ++r.sB; trim_lo(keys, r.sB, r.eB, r.tlB); }
+}
+
+constexpr int kBandGroup = 2;
+constexpr int kUnionSmall = 8;     // union windows this small are shared by the tile      // bands resolved together (loads in flight)
+
+// Light pass.  A warp takes 32 consecutive queries (lane = query): each lane
+// resolves its windows in every band (table half-width, directory, exact
+// trim; kBandGroup bands at a time so their loads overlap) into a segment
+// list in shared memory.  The warp then splits the concatenation of all 32
+// candidate lists evenly over its lanes; candidate k of query q owns staging
+// slot base + excl(q) + k and receives the neighbour id on a hit, -1
+// otherwise, so every lane does the same amount of work and the row order is
+// the candidate order whoever tests it.  Candidates are fetched 4 at a time.
+// Queries with more than kLightMax candidates or kSegCap segments are
+// deferred to k_heavy.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(kLightThreads) k_light(QueryArgs A) {
+__global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
   __shared__ Band sb[kMaxBands];
   __shared__ QMap qm;
   __shared__ int2 segs[kSegCap][kLightThreads];
+  __shared__ int32_t s_c[kLightThreads], s_n[kLightThreads], s_v[kLightThreads];
+  __shared__ int32_t s_hits[kLightThreads];
   load_qmap(A, qm, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
+  const int wb = tid - lane;  // first thread of this warp
   const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -455,38 +532,111 @@ __global__ void __launch_bounds__(kLightThreads) k_light(QueryArgs A) {
     const int64_t t = tile + lane;
     const bool active = t < total_q;
     const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
-    QFull f = load_query<kSampleIds>(A, v);
     int nseg = 0;
     int32_t c = 0;
     bool ovf = false;
-    if (active) {
-      for (int j = 0; j < A.L; ++j) {
-        int32_t sA, eA, sB, eB;
-        band_window(A, sb[j], f.v, sA, eA, sB, eB);
-        if (eA > sA) {
-          if (nseg < kSegCap) segs[nseg++][tid] = make_int2(sA, eA - sA); else ovf = true;
-          c += eA - sA;
+    const double phi = active ? A.q.phi[v] : 0.0;
+    const float rvq = active ? A.q.rf[v] : 3.0e38f;
+    // ---- tile-level union windows (lane = band): the 32 queries are
+    // angular neighbours, so in bands where their windows are wide relative
+    // to the tile's angular span one resolution serves all of them.  Bands
+    // whose union holds <= kUnionSmall candidates (usually none) are handed
+    // to every query as is; the others are resolved per query.
+    unsigned cheap = 0;
+    int32_t uA = 0, uAe = 0, uB = 0, uBe = 0;
+    {
+      double pmin = active ? phi : 1e300, pmax = active ? phi : -1e300;
+      float rmin = rvq;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        pmin = fmin(pmin, __shfl_xor_sync(FULL, pmin, o));
+        pmax = fmax(pmax, __shfl_xor_sync(FULL, pmax, o));
+        rmin = fminf(rmin, __shfl_xor_sync(FULL, rmin, o));
+      }
+      if (pmax >= pmin && pmax - pmin < 0.5 && lane < A.L) {
+        const float dlt = __ldg(wtab_row(A, rmin) + lane);
+        const double half = 0.5 * (pmax - pmin);
+        RawWin r = raw_window(A, sb[lane], 0.5 * (pmin + pmax),
+                              dlt >= 3.14159265f ? dlt : __double2float_ru((double)dlt + half));
+        const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
+        const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
+        const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
+        finish_trim(A.keys, r, kA0, kA1, kB0);
+        if (r.sB < r.eB && r.sB < r.eA) { r.sA = sb[lane].start; r.eA = sb[lane].end; r.sB = r.eB = 0; }
+        uA = r.sA; uAe = r.eA; uB = r.sB; uBe = r.eB;
+        const int32_t un = (uAe - uA) + (uBe - uB);
+        if (un <= kUnionSmall) cheap = 1;
+      }
+      cheap = __ballot_sync(FULL, cheap != 0);
+    }
+    for (int jg = 0; jg < A.L; jg += kBandGroup) {
+      // union segments of the group's bands, from their lanes
+      int32_t gA[kBandGroup], gAe[kBandGroup], gB[kBandGroup], gBe[kBandGroup];
+#pragma unroll
+      for (int u = 0; u < kBandGroup; ++u) {
+        const int j = min(jg + u, 31);
+        gA[u] = __shfl_sync(FULL, uA, j); gAe[u] = __shfl_sync(FULL, uAe, j);
+        gB[u] = __shfl_sync(FULL, uB, j); gBe[u] = __shfl_sync(FULL, uBe, j);
+      }
+      if (!active) continue;
+      {
+        const float* wrow = wtab_row(A, rvq);
+        RawWin w[kBandGroup];
+#pragma unroll
+        for (int u = 0; u < kBandGroup; ++u) {
+          const int j = jg + u;
+          if (j < A.L && !((cheap >> j) & 1u)) w[u] = raw_window(A, sb[j], phi, __ldg(wrow + j));
+          else w[u] = RawWin{0, 0, 0, 0, 0, kQMask + 1, 0};
         }
-        if (eB > sB) {
-          if (nseg < kSegCap) segs[nseg++][tid] = make_int2(sB, eB - sB); else ovf = true;
-          c += eB - sB;
+        uint64_t kA0[kBandGroup], kA1[kBandGroup], kB0[kBandGroup];
+#pragma unroll
+        for (int u = 0; u < kBandGroup; ++u) {
+          kA0[u] = (w[u].sA < w[u].eA && w[u].tlA) ? __ldg(A.keys + w[u].sA) : 0;
+          kA1[u] = (w[u].sA < w[u].eA && w[u].thA <= kQMask) ? __ldg(A.keys + w[u].eA - 1) : 0;
+          kB0[u] = (w[u].sB < w[u].eB && w[u].tlB) ? __ldg(A.keys + w[u].sB) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBandGroup; ++u) {
+          const int j = jg + u;
+          if (j >= A.L) continue;
+          RawWin& r = w[u];
+          if ((cheap >> j) & 1u) {
+            r.sA = gA[u]; r.eA = gAe[u]; r.sB = gB[u]; r.eB = gBe[u];
+          } else {
+            finish_trim(A.keys, r, kA0[u], kA1[u], kB0[u]);
+            if (r.sB < r.eB && r.sB < r.eA) {  // window wraps onto itself: whole band
+              r.sA = sb[j].start; r.eA = sb[j].end; r.sB = r.eB = 0;
+            }
+          }
+          if (r.eA > r.sA) {
+            if (nseg < kSegCap) segs[nseg++][tid] = make_int2(r.sA, r.eA - r.sA); else ovf = true;
+            c += r.eA - r.sA;
+          }
+          if (r.eB > r.sB) {
+            if (nseg < kSegCap) segs[nseg++][tid] = make_int2(r.sB, r.eB - r.sB); else ovf = true;
+            c += r.eB - r.sB;
+          }
         }
       }
     }
     cand_local += (unsigned long long)c;
     const bool heavy = active && (c > kLightMax || ovf);
-    // staging slices: warp-aggregated allocation for light queries
-    int32_t want = (active && !heavy) ? c : 0;
+    const int32_t want = (active && !heavy) ? c : 0;
     int32_t incl = want;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int32_t y = __shfl_up_sync(FULL, incl, o);
       if (lane >= o) incl += y;
     }
+    const int32_t T = __shfl_sync(FULL, incl, 31);
+    const int32_t excl = incl - want;
     unsigned long long base = 0;
-    if (lane == 31 && incl > 0) base = atomicAdd(A.bump, (unsigned long long)incl);
+    if (lane == 31 && T > 0) base = atomicAdd(A.bump, (unsigned long long)T);
     base = __shfl_sync(FULL, base, 31);
-    if (!active) continue;
+    s_c[tid] = want;
+    s_n[tid] = nseg;
+    s_v[tid] = v;
+    s_hits[tid] = 0;
     if (heavy) {
       unsigned long long hoff = atomicAdd(A.bump, (unsigned long long)c);
       unsigned e = atomicAdd(A.heavy_n, 1u);
@@ -494,25 +644,80 @@ __global__ void __launch_bounds__(kLightThreads) k_light(QueryArgs A) {
       A.heavy_c[e] = c;
       A.heavy_of[v] = (int32_t)e;
       A.stage_off[v] = (int64_t)hoff;
-      continue;
+      A.slots[v] = c;
+    } else if (active) {
+      A.heavy_of[v] = -1;
+      A.stage_off[v] = (int64_t)base + excl;
+      A.slots[v] = c;
     }
-    const int64_t off = (int64_t)base + incl - want;
-    A.heavy_of[v] = -1;
-    A.stage_off[v] = off;
-    if (off + c > A.stage_cap) { atomicOr(A.overflow, 1); A.deg[f.idv] = 0; continue; }
-    int32_t* out = A.stage + off;
-    int32_t hits = 0;
-    int k = 0;
-    int2 sg = make_int2(0, 0);
-    if (nseg > 0) sg = segs[0][tid];
-    for (int32_t i = 0; i < c; ++i) {
-      while (sg.y == 0) sg = segs[++k][tid];
-      const int32_t w = sg.x;
-      sg.x++; sg.y--;
-      int32_t idw;
-      if (pair_test<kSampleIds>(f, load_rec(A.rec + w), w, &idw)) out[hits++] = idw;
+    const bool fits = (int64_t)base + T <= A.stage_cap;
+    if (!fits && lane == 0) atomicOr(A.overflow, 1);
+    __syncwarp();
+    // ---- balanced walk over the warp's flattened candidates
+    const int32_t f0 = (int32_t)(((int64_t)T * lane) >> 5);
+    const int32_t f1 = (int32_t)(((int64_t)T * (lane + 1)) >> 5);
+    int q = 0;  // largest lane with excl <= f0
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      int32_t ex = __shfl_sync(FULL, excl, q + st);
+      if (ex <= f0) q += st;
     }
-    A.deg[f.idv] = hits;
+    const int32_t q_excl = __shfl_sync(FULL, excl, q);
+    if (fits && f0 < f1) {
+      int32_t k = f0 - q_excl;  // offset inside query q's candidates
+      int sidx = 0;
+      int2 sg = segs[0][wb + q];
+      while (k >= sg.y) { k -= sg.y; sg = segs[++sidx][wb + q]; }
+      int nq = s_n[wb + q];
+      QFull f = load_query<kSampleIds>(A, s_v[wb + q]);
+      int32_t hits = 0;
+      int32_t* out = A.stage + base;
+      int32_t i = f0;
+      while (i < f1) {
+        int32_t wv[4];
+        int nb = 0;
+        bool qdone = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!qdone && i + nb < f1) {
+            wv[u] = sg.x + k;
+            ++nb;
+            if (++k == sg.y) {
+              k = 0;
+              if (++sidx < nq) sg = segs[sidx][wb + q]; else qdone = true;
+            }
+          }
+        }
+        Rec r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nb) r[u] = load_rec(A.rec + wv[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (u < nb) {
+            int32_t idw;
+            const bool hit = pair_test<kSampleIds>(f, r[u], wv[u], &idw);
+            out[i + u] = hit ? idw : -1;
+            hits += hit;
+          }
+        }
+        i += nb;
+        if (qdone && i < f1) {
+          atomicAdd(&s_hits[wb + q], hits);
+          hits = 0;
+          do { ++q; } while (s_c[wb + q] == 0);
+          sidx = 0;
+          k = 0;
+          sg = segs[0][wb + q];
+          nq = s_n[wb + q];
+          f = load_query<kSampleIds>(A, s_v[wb + q]);
+        }
+      }
+      atomicAdd(&s_hits[wb + q], hits);
+    }
+    __syncwarp();
+    if (active && !heavy) A.deg[kSampleIds ? rec_id(A.rec + v) : v] = fits ? s_hits[tid] : 0;
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand_local += __shfl_xor_sync(FULL, cand_local, o);
@@ -549,7 +754,10 @@ __global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
     const int64_t local = c - A.chunk_start[e];
     QFull f = load_query<kSampleIds>(A, v);
     int32_t sA = 0, eA = 0, sB = 0, eB = 0;
-    if (lane < A.L) band_window(A, sb[lane], f.v, sA, eA, sB, eB);
+    if (lane < A.L) {
+      const float* wrow = wtab_row(A, A.q.rf[v]);
+      band_segments(A, sb[lane], A.q.phi[v], __ldg(wrow + lane), sA, eA, sB, eB);
+    }
     const int32_t lenA = eA - sA, cnt = lenA + (eB - sB);
     int32_t incl = cnt;
 #pragma unroll
@@ -619,7 +827,6 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&x)[E], int lane) {
           int32_t y = __shfl_xor_sync(0xffffffffu, x[t], lj);
           const bool up = (e & k) == 0;
           const bool lower = (e & j) == 0;
-          // keep min if (lower == up) else max
           x[t] = (lower == up) ? min(x[t], y) : max(x[t], y);
         }
       } else {
@@ -639,17 +846,56 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&x)[E], int lane) {
   }
 }
 
+// Bitonic network over a register array (compile-time indices throughout).
+template <int N>
+__device__ __forceinline__ void reg_bitonic(int32_t (&x)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int32_t a = x[i], b = x[l];
+          if ((i & k) == 0) { x[i] = min(a, b); x[l] = max(a, b); }
+          else { x[i] = max(a, b); x[l] = min(a, b); }
+        }
+      }
+    }
+  }
+}
+
+// Misses (-1) sort to the end; hits are non-negative ids.
+__device__ __forceinline__ int32_t miss_last(int32_t x) { return x < 0 ? INT32_MAX : x; }
+
+// Register network over one row's slots held in shared memory: ids
+// ascending, misses (-1) last; the first `len` values are the row, written
+// back in place.  In angular order ids are the candidates' positions, already
+// ascending, so this is an order-preserving compaction; in sample order it is
+// hrgen's sorted row (graph.py:69-71).
+template <int N>
+__device__ __forceinline__ void thread_sort_smem(int32_t* sm, int32_t ns, int32_t len) {
+  int32_t x[N];
+#pragma unroll
+  for (int t = 0; t < N; ++t) x[t] = t < ns ? miss_last(sm[t]) : INT32_MAX;
+  reg_bitonic<N>(x);
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (t < len) sm[t] = x[t];
+}
+
 template <int E>
-__device__ __forceinline__ void copy_sorted_row(const int32_t* __restrict__ src,
-                                                int32_t* __restrict__ dst, int32_t len,
-                                                int lane) {
+__device__ __forceinline__ void warp_sort_slots(const int32_t* src, int32_t ns, int32_t* dst,
+                                                int32_t len, int lane) {
   int32_t x[E];
 #pragma unroll
   for (int t = 0; t < E; ++t) {
     const int e = lane * E + t;
-    x[t] = e < len ? __ldg(src + e) : INT32_MAX;
+    x[t] = e < ns ? miss_last(src[e]) : INT32_MAX;
   }
   warp_bitonic<E>(x, lane);
+  __syncwarp();  // in-place jobs: every lane has read before anyone writes
 #pragma unroll
   for (int t = 0; t < E; ++t) {
     const int e = lane * E + t;
@@ -657,19 +903,59 @@ __device__ __forceinline__ void copy_sorted_row(const int32_t* __restrict__ src,
   }
 }
 
-// Compaction of light rows: a warp owns 32 consecutive queries and moves
-// their rows, one row at a time 32 lanes wide, from the staging slices to
-// the CSR slots rowptr[id].  With sample-order ids the row is sorted on the
-// way through (registers + shuffles), which is the order hrgen's Graph keeps.
+// Sort job: ns slots at src (stage, or the row itself when in place) ->
+// the first len sorted values to dst.
+struct SortJobs {
+  int64_t* src;    // offset into stage, or -1: sort idx[dst .. dst+len) in place
+  int64_t* dst;
+  int32_t* ns;
+  int32_t* len;
+  unsigned* n;     // queued jobs
+  unsigned* nbig;  // jobs above kWarpSortMax slots, for k_sort_block
+  int32_t* big;    // their job indices
+  unsigned* nhuge; // in-place rows above kBucketMax: segmented sort
+  int64_t* huge_b;
+  int64_t* huge_e;
+};
+
+constexpr int kWarpSortMax = 256;
+
+// Queue a sort job; called by every lane of a warp (want = this lane has a
+// job), one atomic per warp.
+__device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int64_t src,
+                                              int64_t dst, int32_t ns, int32_t len) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(FULL, want);
+  if (!bal) return;
+  unsigned base = 0;
+  if (lane == __ffs(bal) - 1) base = atomicAdd(J.n, (unsigned)__popc(bal));
+  base = __shfl_sync(FULL, base, __ffs(bal) - 1);
+  if (want) {
+    const unsigned k = base + __popc(bal & ((1u << lane) - 1u));
+    J.src[k] = src; J.dst[k] = dst; J.ns[k] = ns; J.len[k] = len;
+  }
+}
+
+constexpr int kCompactThreads = 128;
+constexpr int kSmallSlots = 64;                 // rows sorted by one thread
+constexpr int kTileSlots = 32 * kSmallSlots;    // smem slots per warp
+
+// Compaction of light rows.  A warp owns the same 32 consecutive queries as
+// in k_light, whose staging slices are contiguous: rows of <= kSmallSlots
+// slots are loaded coalesced into shared memory, each lane sorts its row with
+// a register network (misses last), and the warp writes the rows out one by
+// one, 32 lanes wide.  Longer rows are queued for k_sort_warp / k_sort_block.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(256) k_compact_light(QueryArgs A,
-                                                       const int64_t* __restrict__ rowptr,
-                                                       int32_t* __restrict__ idx) {
+__global__ void __launch_bounds__(kCompactThreads) k_compact_light(
+    QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
   __shared__ Band sb[kMaxBands];
   __shared__ QMap qm;
+  __shared__ int32_t buf[kCompactThreads / 32][kTileSlots];
   load_qmap(A, qm, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  int32_t* sm = buf[threadIdx.x >> 5];
   const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -677,45 +963,193 @@ __global__ void __launch_bounds__(256) k_compact_light(QueryArgs A,
     const int64_t t = tile + lane;
     const bool active = t < total_q;
     const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
-    const int32_t idv = kSampleIds ? (int32_t)(__double_as_longlong(__ldg(
-                                         reinterpret_cast<const double*>(A.rec + v) + 5)) &
-                                     0xffffffffll)
-                                   : v;
     const bool light = active && A.heavy_of[v] < 0;
-    const int64_t dst = light ? rowptr[idv] : 0;
-    const int32_t len = light ? (int32_t)(rowptr[idv + 1] - dst) : 0;
-    const int64_t src = light ? A.stage_off[v] : 0;
-    unsigned todo = __ballot_sync(FULL, len > 0);
+    int32_t ns = 0, len = 0;
+    int64_t dst = 0, src = 0;
+    if (light) {
+      const int32_t idv = kSampleIds ? rec_id(A.rec + v) : v;
+      dst = rowptr[idv];
+      len = (int32_t)(rowptr[idv + 1] - dst);
+      ns = A.slots[v];
+      src = A.stage_off[v];
+    }
+    const bool small = len > 0 && ns <= kSmallSlots;
+    push_job_warp(J, len > 0 && !small, src, dst, ns, len);
+    // pack the small rows' slices into shared memory: lane offsets by scan
+    const int32_t want = small ? ns : 0;
+    int32_t incl = want;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int32_t excl = incl - want;
+    unsigned todo = __ballot_sync(FULL, small);
+    {
+      unsigned rows = todo;
+      while (rows) {  // copy each small slice (<= 64 slots) with the whole warp
+        const int l = __ffs(rows) - 1;
+        rows &= rows - 1;
+        const int64_t s0 = __shfl_sync(FULL, src, l);
+        const int32_t n0 = __shfl_sync(FULL, ns, l), e0 = __shfl_sync(FULL, excl, l);
+        for (int k = lane; k < n0; k += 32) sm[e0 + k] = __ldg(A.stage + s0 + k);
+      }
+    }
+    __syncwarp();
+    const int32_t mx = __reduce_max_sync(FULL, want);
+    if (mx <= 16) {
+      if (small) thread_sort_smem<16>(sm + excl, ns, len);
+    } else if (mx <= 32) {
+      if (small) thread_sort_smem<32>(sm + excl, ns, len);
+    } else {
+      if (small) thread_sort_smem<64>(sm + excl, ns, len);
+    }
+    __syncwarp();
     while (todo) {
       const int l = __ffs(todo) - 1;
       todo &= todo - 1;
       const int64_t d = __shfl_sync(FULL, dst, l);
-      const int32_t ln = __shfl_sync(FULL, len, l);
-      const int64_t s0 = __shfl_sync(FULL, src, l);
-      const int32_t* in = A.stage + s0;
-      int32_t* out = idx + d;
-      if (!kSampleIds) {
-        int32_t x[8];
+      const int32_t n0 = __shfl_sync(FULL, len, l), e0 = __shfl_sync(FULL, excl, l);
+      for (int k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
+    }
+    __syncwarp();
+  }
+}
+
+// Queued rows.  Angular ids (kSorted == false): candidate order is id order,
+// so a row is just its hits in slot order -- an O(P) ballot compaction, any
+// length.  Sample ids: rows of up to kWarpSortMax slots are sorted by one
+// warp in registers; longer ones go to k_sort_block.
+template <bool kSorted>
+__global__ void __launch_bounds__(256) k_sort_warp(const int32_t* __restrict__ stage,
+                                                   int32_t* __restrict__ idx, SortJobs J) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned nj = *J.n;
+  for (int64_t k = warp; k < nj; k += nwarps) {
+    const int64_t s0 = J.src[k], d = J.dst[k];
+    const int32_t ns = J.ns[k], len = J.len[k];
+    const int32_t* src = s0 >= 0 ? stage + s0 : idx + d;
+    int32_t* dst = idx + d;
+    if (!kSorted) {
+      const unsigned lt = (1u << lane) - 1u;
+      int32_t put = 0;
+      for (int32_t k0 = 0; k0 < ns; k0 += 128) {
+        int32_t x[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int k = lane + 32 * u;
-          x[u] = k < ln ? __ldg(in + k) : 0;
+        for (int u = 0; u < 4; ++u) {
+          const int i = k0 + 32 * u + lane;
+          x[u] = i < ns ? __ldg(src + i) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int k = lane + 32 * u;
-          if (k < ln) out[k] = x[u];
+        for (int u = 0; u < 4; ++u) {
+          const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
+          if (x[u] >= 0) dst[put + __popc(bal & lt)] = x[u];
+          put += __popc(bal);
         }
-      } else if (ln <= 32) {
-        copy_sorted_row<1>(in, out, ln, lane);
-      } else if (ln <= 64) {
-        copy_sorted_row<2>(in, out, ln, lane);
-      } else if (ln <= 128) {
-        copy_sorted_row<4>(in, out, ln, lane);
-      } else {
-        copy_sorted_row<8>(in, out, ln, lane);
+      }
+      continue;
+    }
+    if (ns <= 64) warp_sort_slots<2>(src, ns, dst, len, lane);
+    else if (ns <= 128) warp_sort_slots<4>(src, ns, dst, len, lane);
+    else if (ns <= kWarpSortMax) warp_sort_slots<8>(src, ns, dst, len, lane);
+    else if (lane == 0) J.big[atomicAdd(J.nbig, 1u)] = (int32_t)k;  // one per long row
+  }
+}
+
+constexpr int kBucketMax = 4096;   // slots a block bucket sort handles
+constexpr int kBucketThreads = 256;
+constexpr int kPerThread = kBucketMax / kBucketThreads;
+
+// Jobs above kWarpSortMax slots: one block per job, O(P) bucket sort in shared
+// memory.  Ids are i.i.d. uniform over [0, n) (vertex order = draw order), so
+// P/4 value buckets hold ~4 ids each; misses go to a last bucket.  Buckets
+// are then finished by insertion sort.  Jobs above kBucketMax slots (hub rows,
+// in place) are left to a segmented sort.
+__global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __restrict__ stage,
+                                                               int32_t* __restrict__ idx,
+                                                               SortJobs J, int64_t n_ids) {
+  __shared__ int32_t out[kBucketMax];
+  __shared__ int32_t cnt[kBucketMax / 4 + 2];
+  __shared__ int32_t wsum[kBucketThreads / 32];
+  const unsigned nb = *J.nbig;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
+    const int32_t k = J.big[r];
+    const int32_t ns = J.ns[k], len = J.len[k];
+    const int64_t s0 = J.src[k], d = J.dst[k];
+    if (ns > kBucketMax) {
+      if (tid == 0) {
+        const unsigned h = atomicAdd(J.nhuge, 1u);
+        J.huge_b[h] = d;
+        J.huge_e[h] = d + len;
+      }
+      continue;
+    }
+    const int32_t* src = s0 >= 0 ? stage + s0 : idx + d;
+    int B = 1;
+    while (4 * B < ns) B <<= 1;  // value buckets; bucket B holds the misses
+    const float scale = (float)B / (float)n_ids;
+    for (int b = tid; b <= B; b += kBucketThreads) cnt[b] = 0;
+    __syncthreads();
+    int32_t x[kPerThread];
+    int16_t bk[kPerThread];
+#pragma unroll
+    for (int u = 0; u < kPerThread; ++u) {
+      const int i = tid + u * kBucketThreads;
+      x[u] = i < ns ? src[i] : -1;
+      bk[u] = -1;
+      if (i < ns) {
+        bk[u] = x[u] < 0 ? (int16_t)B : (int16_t)min((int)((float)x[u] * scale), B - 1);
+        atomicAdd(&cnt[bk[u]], 1);
       }
     }
+    __syncthreads();
+    // exclusive scan of cnt[0..B] (B + 1 <= 1025 entries, 256 threads)
+    {
+      const int per = (B + 1 + kBucketThreads - 1) / kBucketThreads;
+      int32_t acc = 0;
+      for (int q = 0; q < per; ++q) {
+        const int b = tid * per + q;
+        if (b <= B) acc += cnt[b];
+      }
+      int32_t inc = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      int32_t woff = 0;
+      for (int w = 0; w < warp; ++w) woff += wsum[w];
+      int32_t run = woff + inc - acc;
+      for (int q = 0; q < per; ++q) {
+        const int b = tid * per + q;
+        if (b <= B) { const int32_t c = cnt[b]; cnt[b] = run; run += c; }
+      }
+    }
+    __syncthreads();
+    // scatter (order inside a bucket is fixed below)
+#pragma unroll
+    for (int u = 0; u < kPerThread; ++u)
+      if (bk[u] >= 0) out[atomicAdd(&cnt[bk[u]], 1)] = x[u];
+    __syncthreads();
+    // cnt[b] is now the end of bucket b; insertion-sort each value bucket
+    for (int b = tid; b < B; b += kBucketThreads) {
+      const int beg = b == 0 ? 0 : cnt[b - 1], end = cnt[b];
+      for (int i = beg + 1; i < end; ++i) {
+        const int32_t v = out[i];
+        int j = i - 1;
+        while (j >= beg && out[j] > v) { out[j + 1] = out[j]; --j; }
+        out[j + 1] = v;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < len; i += kBucketThreads) idx[d + i] = out[i];
+    __syncthreads();
   }
 }
 
@@ -737,10 +1171,7 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
     }
     const int64_t e = lo;
     const int32_t v = A.heavy_v[e];
-    const int32_t idv = sample_ids ? (int32_t)(__double_as_longlong(__ldg(
-                                         reinterpret_cast<const double*>(A.rec + v) + 5)) &
-                                     0xffffffffll)
-                                   : v;
+    const int32_t idv = sample_ids ? rec_id(A.rec + v) : v;
     const int64_t c0 = A.chunk_start[e];
     const int64_t d = rowptr[idv] + (chunk_off[c] - chunk_off[c0]);
     const int32_t h = A.chunk_hits[c];
@@ -761,27 +1192,42 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
   }
 }
 
-// begin/end offsets of the heavy rows (sample-order ids: these rows still
-// need sorting after the chunk-parallel copy)
-__global__ void k_heavy_segments(QueryArgs A, int64_t H, const int64_t* __restrict__ rowptr,
-                                 int64_t* __restrict__ seg_begin, int64_t* __restrict__ seg_end) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= H) return;
-  const int32_t v = A.heavy_v[e];
-  const int32_t idv = (int32_t)(__double_as_longlong(
-                                    __ldg(reinterpret_cast<const double*>(A.rec + v) + 5)) &
-                                0xffffffffll);
-  seg_begin[e] = rowptr[idv];
-  seg_end[e] = rowptr[idv + 1];
+// Sample-order ids: heavy rows arrive in (band, angle) order of their
+// neighbours; queue each for an in-place sort.
+__global__ void k_queue_heavy_rows(QueryArgs A, int64_t H, const int64_t* __restrict__ rowptr,
+                                   SortJobs J) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t b = 0;
+  int32_t len = 0;
+  if (e < H) {
+    const int32_t idv = rec_id(A.rec + A.heavy_v[e]);
+    b = rowptr[idv];
+    len = (int32_t)(rowptr[idv + 1] - b);
+  }
+  push_job_warp(J, len > 1, -1, b, len, len);
 }
 
-__global__ void __launch_bounds__(256) k_copy_segments(const int32_t* __restrict__ from,
-                                                       int32_t* __restrict__ to,
-                                                       const int64_t* __restrict__ b,
-                                                       const int64_t* __restrict__ e,
-                                                       int64_t H) {
-  for (int64_t s = blockIdx.x; s < H; s += gridDim.x)
-    for (int64_t k = b[s] + threadIdx.x; k < e[s]; k += blockDim.x) to[k] = from[k];
+__global__ void __launch_bounds__(1024) k_copy_segments(const int32_t* __restrict__ from,
+                                                        int32_t* __restrict__ to,
+                                                        const int64_t* __restrict__ b,
+                                                        const int64_t* __restrict__ e,
+                                                        int64_t H) {
+  for (int64_t s = blockIdx.x; s < H; s += gridDim.x) {
+    const int64_t lo = b[s], hi = e[s];
+    for (int64_t k0 = lo; k0 < hi; k0 += 8 * 1024) {
+      int32_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = k0 + u * 1024 + threadIdx.x;
+        x[u] = k < hi ? from[k] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t k = k0 + u * 1024 + threadIdx.x;
+        if (k < hi) to[k] = x[u];
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,
