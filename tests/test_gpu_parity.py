@@ -186,14 +186,19 @@ def test_angular_order_is_a_relabelling(oracle):
 
 
 def test_shards_partition_the_rows():
+    from paper_1501_03545_b200 import distributed as D
     p = GeneratorParams(n=200_000, avg_degree=16.0, gamma=2.5, seed=9)
     full = P.generate(p)
+    model = p.resolve()
+    co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    sector = D.sector_of(co.phi, 4)
     acc_rows = np.zeros(full.n, np.int64)
     parts = []
     for k in range(4):
         g, st = P.generate_with_stats(p, shard=P.Shard(k, 4))
         deg = np.diff(g.indptr)
         assert np.all(acc_rows[deg > 0] == 0)   # disjoint row sets
+        assert np.all(sector[deg > 0] == k)     # device sectors == host mirror
         acc_rows += deg
         parts.append(g)
     assert np.array_equal(acc_rows, np.diff(full.indptr))
