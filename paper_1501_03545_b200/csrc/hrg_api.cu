@@ -178,8 +178,9 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   }
   k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>());
-  k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(),
-                                               c->s_bf.as<float>(), c->bands.as<Band>());
+  k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(
+      n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(), c->s_bf.as<float>(),
+      c->s_rp.as<double>(), c->bands.as<Band>());
   k_band_finish<<<1, 64, 0, st>>>(c->bands.as<Band>(), L);
   k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
                                             c->dir.as<int32_t>());
@@ -243,9 +244,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(c->wtab.ensure(sizeof(float) * (size_t)rows * L));
   A.wtab = c->wtab.as<float>();
   A.wrows = rows;
-  const double E_over_tanh = std::ldexp(1.0, -45) / std::tanh(M->R) * 1.001;
-  k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->R, M->cosh_r_minus_1, E_over_tanh,
-                                      c->wtab.as<float>());
+  k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->cosh_r_minus_1,
+                                      std::ldexp(1.0, -45), c->wtab.as<float>());
   int launches = 1;
 
   if (c->grid_light == 0) {

@@ -42,6 +42,7 @@ struct Band {
   float bmin;              // min (1-r)(1+r) in band (rounded down)
   float sinh_rmin;
   float pad_;
+  double pmin;             // innermost Poincare radius of the band's points
 };
 
 struct BandSpec {          // band(rp) = #{ j in [1, L) : thr[j] <= rp }
@@ -198,6 +199,7 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     B.bmin = __int_as_float(0x7f800000);
     B.sinh_rmin = 0.f;
     B.pad_ = 0.f;
+    B.pmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf until k_band_minmax
     B.dir_base = 0;
     bands[j] = B;
   }
@@ -215,9 +217,14 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
 __global__ void __launch_bounds__(256) k_band_minmax(int64_t n, const uint64_t* __restrict__ keys,
                                                      const float* __restrict__ rf,
                                                      const float* __restrict__ bf,
+                                                     const double* __restrict__ s_rp,
                                                      Band* __restrict__ bands) {
   __shared__ int sr[kMaxBands], sbm[kMaxBands];
-  if (threadIdx.x < kMaxBands) { sr[threadIdx.x] = 0x7f800000; sbm[threadIdx.x] = 0x7f800000; }
+  __shared__ unsigned long long sp[kMaxBands];
+  if (threadIdx.x < kMaxBands) {
+    sr[threadIdx.x] = 0x7f800000; sbm[threadIdx.x] = 0x7f800000;
+    sp[threadIdx.x] = 0x7ff0000000000000ull;
+  }
   __syncthreads();
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -230,11 +237,14 @@ __global__ void __launch_bounds__(256) k_band_minmax(int64_t n, const uint64_t* 
       atomicMin(&sr[band], rm);
       atomicMin(&sbm[band], bm);
     }
+    // non-negative doubles order like their bit patterns
+    atomicMin(&sp[band], (unsigned long long)__double_as_longlong(s_rp[p]));
   }
   __syncthreads();
   if (threadIdx.x < kMaxBands && sr[threadIdx.x] != 0x7f800000) {
     atomicMin((int*)&bands[threadIdx.x].rmin, sr[threadIdx.x]);
     atomicMin((int*)&bands[threadIdx.x].bmin, sbm[threadIdx.x]);
+    atomicMin(reinterpret_cast<unsigned long long*>(&bands[threadIdx.x].pmin), sp[threadIdx.x]);
   }
 }
 
@@ -311,38 +321,58 @@ __device__ __forceinline__ void trim_hi(const uint64_t* keys, int32_t s, int32_t
   while (e > s && (__ldg(keys + e - 1) & kQMask) > qh) --e;
 }
 
-// Half-width of the angular window in which band B can hold a vertex within
-// hyperbolic distance R + eta of a query at radius >= rq whose (1-r)(1+r) is
-// >= bq.  eta bounds the fp64 decision noise of the reference predicate for
-// the pair in either orientation, so no pair the
-// predicate accepts falls outside.  Returns >= pi for "the whole band".
-__device__ __forceinline__ double window_halfwidth(double R, double a, double E_over_tanh, double rq,
-                                                   double bq, double rb, double bb) {
+// ------------------------------------------------------------ window table
+//
+// For query v (Poincare radius r, circle centre c, radius rad from
+// geometry.py:141-157) and a point w at Poincare radius p >= p1 and angle
+// offset psi, hrgen's exact test is |P_w - C_v|^2 - rad^2 < 0 with
+// |P_w - C_v|^2 = p^2 + c^2 - 2pc cos psi.  With F = 2|P_v-P_w|^2 - a b_v b_w
+// (b = (1-r)(1+r), D = a b + 2) one has |P_w - C_v|^2 - rad_v^2 = F / D_v, and
+// the fp64 evaluation of either orientation of the predicate errs by at most
+// e = 2^-45 in its own frame (all operands <= 1 in magnitude), so a pair that
+// either orientation accepts has F < e * max(D_v, D_w), i.e. in v's frame
+//   cos psi > (p^2 + c^2 - rad^2 - e * max(1, D_w / D_v)) / (2 p c).
+// The right side increases with p (c^2 - rad^2 < 0: every query circle holds
+// the origin), so p = p1, the band's innermost point, bounds the window; D_w
+// is largest there and D_v smallest at the row's outer edge.  The pad is a
+// fixed fraction of the window's size in cos-space across bands (both scale
+// like e^(r_v - r_w)), so windows stay tight at every disk radius.
+__device__ __forceinline__ double poincare_halfwidth(double a, double e, double r_native,
+                                                     double p1) {
   const double pi = 3.141592653589793;
-  const double eta = E_over_tanh * (1.0 / fmin(bq, bb) + 2.0 / (a * bq * bb)) + 3e-5;
-  const double Rp = R + fmin(eta, 64.0);
-  if (rq + rb <= Rp) return 4.0;
-  // cosh R' = cosh(rq - rb) + 2 sinh rq sinh rb sin^2(d/2) at the widest point
-  const double s2 = (cosh(Rp) - cosh(rq - rb)) / (2.0 * sinh(rq) * sinh(rb));
-  if (!(s2 < 1.0)) return 4.0;
-  const double d = 2.0 * asin(sqrt(fmax(s2, 0.0))) * (1.0 + 1e-6) + 1e-13;
+  const double rh = tanh(0.5 * r_native);
+  const double b = (1.0 - rh) * (1.0 + rh);
+  const double denom = a * b + 2.0;
+  const double c = 2.0 * rh / denom;
+  const double diff = (2.0 * rh * rh - a * b) / denom;  // c^2 - rad^2, without cancellation
+  if (!(p1 * c > 0.0)) return diff - e < 0.0 ? 4.0 : -1.0;
+  const double cl = (p1 * p1 + diff - e) / (2.0 * p1 * c);
+  if (cl <= -1.0) return 4.0;
+  if (cl >= 1.0) return -1.0;
+  const double d = acos(cl) * (1.0 + 1e-9) + 1e-15;
   return d >= pi ? 4.0 : d;
 }
 
-// Window table: row s covers query radii [s*kRowStep, (s+1)*kRowStep).
-__global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, double R,
-                               double a, double E_over_tanh, float* __restrict__ wtab) {
+// Row s covers query (hyperbolic) radii [s*kRowStep, (s+1)*kRowStep); entry
+// < 0: no vertex of the band can be a neighbour; >= pi: the whole band.
+__global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, double a,
+                               double E, float* __restrict__ wtab) {
   const int s = blockIdx.x, j = threadIdx.x;
   if (s >= rows || j >= L) return;
   const Band B = bands[j];
-  float out = 0.0f;
+  float out = -1.0f;
   if (B.end > B.start) {
-    const double rq = s * (double)kRowStep;
-    // (1-r)(1+r) = 1/cosh^2(r/2) is smallest at the row's top (+ fp32 slack)
-    const double ch = cosh(0.5 * (rq + kRowStep + 1e-5));
-    const double bq = 0.99 / (ch * ch);
-    const double d = window_halfwidth(R, a, E_over_tanh, rq, bq, (double)B.rmin, (double)B.bmin);
-    out = __double2float_ru(d);
+    const double r_lo = s * (double)kRowStep;
+    const double r_hi = (s + 1) * (double)kRowStep + 1e-5;  // + fp32 slack of the row index
+    const double ch = cosh(0.5 * r_hi);
+    const double Dv = a * (0.99 / (ch * ch)) + 2.0;       // smallest D of the row's queries
+    const double bw = (1.0 - B.pmin) * (1.0 + B.pmin);
+    const double Dw = a * bw + 2.0;                       // largest D of the band's points
+    const double e = E * fmax(1.0, Dw / Dv) * 1.01;
+    // the window shrinks across the row; take both ends plus slack
+    const double d = fmax(poincare_halfwidth(a, e, r_lo, B.pmin),
+                          poincare_halfwidth(a, e, r_hi, B.pmin));
+    out = d < 0.0 ? -1.0f : (d >= 3.14159 ? 4.0f : __double2float_ru(d * 1.01));
   }
   wtab[s * L + j] = out;
 }
@@ -353,7 +383,7 @@ __device__ __forceinline__ void band_segments(const QueryArgs& A, const Band& B,
                                               float dlt_f, int32_t& sA, int32_t& eA,
                                               int32_t& sB, int32_t& eB) {
   sA = eA = sB = eB = 0;
-  if (B.end <= B.start) return;
+  if (B.end <= B.start || dlt_f < 0.0f) return;
   if (dlt_f >= 3.14159265f) { sA = B.start; eA = B.end; return; }
   const double dlt = (double)dlt_f;
   const double lo = phi - dlt, hi = phi + dlt;
@@ -472,7 +502,7 @@ __device__ __forceinline__ RawWin raw_window(const QueryArgs& A, const Band& B, 
   RawWin r;
   r.sA = r.eA = r.sB = r.eB = 0;
   r.tlA = 0; r.thA = kQMask + 1; r.tlB = 0;
-  if (B.end <= B.start) return r;
+  if (B.end <= B.start || dlt_f < 0.0f) return r;
   if (dlt_f >= 3.14159265f) { r.sA = B.start; r.eA = B.end; return r; }
   const double dlt = (double)dlt_f;
   const double lo = phi - dlt, hi = phi + dlt;
@@ -557,7 +587,8 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
         const float dlt = __ldg(wtab_row(A, rmin) + lane);
         const double half = 0.5 * (pmax - pmin);
         RawWin r = raw_window(A, sb[lane], 0.5 * (pmin + pmax),
-                              dlt >= 3.14159265f ? dlt : __double2float_ru((double)dlt + half));
+                              (dlt < 0.0f || dlt >= 3.14159265f)
+                                  ? dlt : __double2float_ru((double)dlt + half));
         const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
         const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
         const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
