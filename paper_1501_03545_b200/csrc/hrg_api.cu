@@ -73,7 +73,7 @@ struct hrg_context {
   // sort
   Buf keys_in, keys_out, vals_in, vals_out;
   // sorted records
-  Buf rec, s_phi, s_rf, s_bf, s_rp, s_rn;
+  Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
       chunk_off, huge_b, huge_e, slots, wtab, job_src, job_dst, job_ns, job_len, job_big;
@@ -127,6 +127,8 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->keys_in.ensure(u64)); CUDA_TRY(c->keys_out.ensure(u64));
   CUDA_TRY(c->vals_in.ensure(i32)); CUDA_TRY(c->vals_out.ensure(i32));
   for (Buf* b : {&c->s_phi, &c->s_rp, &c->s_rn}) CUDA_TRY(b->ensure(d));
+  CUDA_TRY(c->pt.ensure(16 * (size_t)n));
+  CUDA_TRY(c->circ.ensure(sizeof(Circ) * (size_t)n));
   CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
   CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(64));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
@@ -149,7 +151,7 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 // Sort keys -> permutation; build the sorted SoA, band table and directory.
 hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, int L,
-                       const hrg_shard* shard, double C) {
+                       const hrg_shard* shard, double C, bool sample_ids) {
   int64_t n = M->n;
   cudaStream_t st = c->stream;
   int end_bit = kQBits + 6;
@@ -164,10 +166,18 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                                            c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
   CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
   QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
-  k_gather<<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
-                                          c->rp.as<double>(), c->rn.as<double>(),
-                                          M->cosh_r_minus_1, c->rec.as<Rec>(), q,
-                                          c->s_rp.as<double>(), c->s_rn.as<double>());
+  const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
+                  c->vals_out.as<int32_t>()};
+  if (sample_ids)
+    k_gather<true><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
+                                                  c->rp.as<double>(), c->rn.as<double>(),
+                                                  M->cosh_r_minus_1, recs, q,
+                                                  c->s_rp.as<double>(), c->s_rn.as<double>());
+  else
+    k_gather<false><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
+                                                   c->rp.as<double>(), c->rn.as<double>(),
+                                                   M->cosh_r_minus_1, recs, q,
+                                                   c->s_rp.as<double>(), c->s_rn.as<double>());
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     uint64_t span = (uint64_t)1 << kQBits;
@@ -219,7 +229,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   cudaStream_t st = c->stream;
   QueryArgs A;
   memset(&A, 0, sizeof(A));
-  A.rec = c->rec.as<Rec>();
+  A.rec = Recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
+                c->vals_out.as<int32_t>()};
   A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
   A.bands = c->bands.as<Band>();
   A.dir = c->dir.as<int32_t>();
@@ -432,7 +443,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev[E_SAMPLED], st));
-  hrg_status s = build_index(c, M, S, L, shard, C);
+  hrg_status s = build_index(c, M, S, L, shard, C, sample_ids);
   if (s != HRG_OK) return s;
   if (stats) stats->kernel_launches = 7;  // sample/keys, gather, 5 index kernels (+ CUB sort)
   s = emit_edges(c, M, L, C, sample_ids, stats);
@@ -481,7 +492,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
+                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->huge_b,
                  &c->huge_e, &c->slots, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
@@ -594,7 +605,7 @@ hrg_status hrg_sample_points(hrg_context* c, const hrg_model* M, uint64_t seed, 
   CUDA_TRY(cudaGetLastError());
   const double *sp = c->phi.as<double>(), *sn = c->rn.as<double>(), *sr = c->rp.as<double>();
   if (order == HRG_ORDER_ANGULAR) {
-    s = build_index(c, M, S, L, nullptr, C);
+    s = build_index(c, M, S, L, nullptr, C, false);
     if (s != HRG_OK) return s;
     sp = c->s_phi.as<double>(); sn = c->s_rn.as<double>(); sr = c->s_rp.as<double>();
   }

@@ -113,13 +113,27 @@ __global__ void __launch_bounds__(256) k_keys_from_coords(int64_t n, const doubl
   vals[i] = (int32_t)i;
 }
 
-// Candidate record: everything one pair test needs about a vertex w, in one
-// 48-byte line fragment: its point (p_x, p_y) for pred(v -> w), its circle
-// (c_x, c_y, rad^2) for pred(w -> v), and its vertex id.
+// Candidate records, split by orientation so a pair test fetches only what
+// it needs: the point (p_x, p_y) for pred(v -> w), 16 B, or the circle
+// (c_x, c_y, rad^2), 32 B, for pred(w -> v); the vertex id (4 B, the sort
+// permutation) decides which.
+struct __align__(16) Circ {
+  double cx, cy, rsq, pad;
+};
+
+// Sample-order ids: the orientation is known only once w's id is read, so
+// the whole record (both halves + id, 48 B) is fetched in one go instead.
 struct __align__(16) Rec {
   double px, py, cx, cy, rsq;
   int32_t id;
-  float pad;
+  int32_t pad;
+};
+
+struct Recs {
+  double2* pt;          // angular order
+  Circ* circ;           // angular order
+  Rec* rec;             // sample order
+  const int32_t* ids;   // sorted position -> vertex id
 };
 
 struct QRec {          // query-side extras, per sorted position
@@ -131,11 +145,12 @@ struct QRec {          // query-side extras, per sorted position
 // Gather into (band, angle) order and precompute every per-point quantity the
 // query needs.  p_x/p_y: quadtree.py:474-475; c_x/c_y/rad^2: quadtree.py:516-518
 // with center_r/rad from geometry.py:141-157.
+template <bool kSampleIds>
 __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __restrict__ perm,
                                                 const double* __restrict__ phi,
                                                 const double* __restrict__ rp,
                                                 const double* __restrict__ rn, double a,
-                                                Rec* __restrict__ rec, QRec q,
+                                                Recs rec, QRec q,
                                                 double* __restrict__ s_rp,
                                                 double* __restrict__ s_rn) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -146,15 +161,18 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __rest
   sincos_cr(ph, &sn, &cs);
   double cr, rad;
   circle_params(r, a, &cr, &rad);
-  Rec R;
-  R.px = __dmul_rn(r, cs);
-  R.py = __dmul_rn(r, sn);
-  R.cx = __dmul_rn(cr, cs);
-  R.cy = __dmul_rn(cr, sn);
-  R.rsq = __dmul_rn(rad, rad);
-  R.id = i;
-  R.pad = 0.f;
-  rec[p] = R;
+  const double px = __dmul_rn(r, cs), py = __dmul_rn(r, sn);
+  const double cx = __dmul_rn(cr, cs), cy = __dmul_rn(cr, sn), rsq = __dmul_rn(rad, rad);
+  if (kSampleIds) {
+    Rec R;
+    R.px = px; R.py = py; R.cx = cx; R.cy = cy; R.rsq = rsq; R.id = i; R.pad = 0;
+    rec.rec[p] = R;
+  } else {
+    rec.pt[p] = make_double2(px, py);
+    Circ ci;
+    ci.cx = cx; ci.cy = cy; ci.rsq = rsq; ci.pad = 0.0;
+    rec.circ[p] = ci;
+  }
   q.phi[p] = ph;
   // hyperbolic radius of the stored Poincare point and (1-r)(1+r), both
   // rounded down: only used to size conservative angular windows.
@@ -284,7 +302,7 @@ constexpr int kLightThreads = 128;
 constexpr float kRowStep = 1.0f / 16.0f;  // window table: query-radius row height
 
 struct QueryArgs {
-  const Rec* rec;
+  Recs rec;
   QRec q;
   const Band* bands;
   const int32_t* dir;
@@ -418,19 +436,14 @@ __device__ __forceinline__ const float* wtab_row(const QueryArgs& A, float rv) {
   return A.wtab + row * A.L;
 }
 
-__device__ __forceinline__ Rec load_rec(const Rec* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
-  Rec r;
-  r.px = a.x; r.py = a.y; r.cx = b.x; r.cy = b.y; r.rsq = c.x;
-  r.id = (int32_t)(__double_as_longlong(c.y) & 0xffffffffll);
-  r.pad = 0.f;
-  return r;
-}
+__device__ __forceinline__ double2 load_pt(const Recs& R, int32_t w) { return __ldg(R.pt + w); }
 
-__device__ __forceinline__ int32_t rec_id(const Rec* p) {
-  return (int32_t)(__double_as_longlong(__ldg(reinterpret_cast<const double*>(p) + 5)) &
-                   0xffffffffll);
+__device__ __forceinline__ Circ load_circ(const Recs& R, int32_t w) {
+  const double2* q = reinterpret_cast<const double2*>(R.circ + w);
+  const double2 a = __ldg(q), b = __ldg(q + 1);
+  Circ c;
+  c.cx = a.x; c.cy = a.y; c.rsq = b.x; c.pad = 0.0;
+  return c;
 }
 
 struct QFull {
@@ -438,25 +451,69 @@ struct QFull {
   int32_t pos, idv;
 };
 
+__device__ __forceinline__ void load_rec(const Recs& R, int32_t w, double2& a, double2& b,
+                                         double2& c) {
+  const double2* q = reinterpret_cast<const double2*>(R.rec + w);
+  a = __ldg(q); b = __ldg(q + 1); c = __ldg(q + 2);
+}
+
 template <bool kSampleIds>
 __device__ __forceinline__ QFull load_query(const QueryArgs& A, int32_t v) {
   QFull f;
-  Rec r = load_rec(A.rec + v);
-  f.px = r.px; f.py = r.py; f.cx = r.cx; f.cy = r.cy; f.rsq = r.rsq;
   f.pos = v;
-  f.idv = kSampleIds ? r.id : v;
+  if (kSampleIds) {
+    double2 a, b, c;
+    load_rec(A.rec, v, a, b, c);
+    f.px = a.x; f.py = a.y; f.cx = b.x; f.cy = b.y; f.rsq = c.x;
+    f.idv = (int32_t)(__double_as_longlong(c.y) & 0xffffffffll);
+  } else {
+    const double2 p = load_pt(A.rec, v);
+    const Circ c = load_circ(A.rec, v);
+    f.px = p.x; f.py = p.y; f.cx = c.cx; f.cy = c.cy; f.rsq = c.rsq;
+    f.idv = v;
+  }
   return f;
+}
+
+// One candidate's data for its pair test: the circle of w if w's id is the
+// smaller (it decides), else the point of w.
+struct Cand {
+  double d0, d1, d2;
+  int32_t id;
+  bool lower;
+};
+
+template <bool kSampleIds>
+__device__ __forceinline__ Cand load_cand(const QueryArgs& A, const QFull& f, int32_t w) {
+  Cand c;
+  if (kSampleIds) {
+    double2 a, b, x;
+    load_rec(A.rec, w, a, b, x);
+    c.id = (int32_t)(__double_as_longlong(x.y) & 0xffffffffll);
+    c.lower = c.id < f.idv;
+    c.d0 = c.lower ? b.x : a.x;
+    c.d1 = c.lower ? b.y : a.y;
+    c.d2 = x.x;
+  } else {
+    c.id = w;
+    c.lower = w < f.pos;  // angular ids are positions
+    if (c.lower) {
+      const Circ ci = load_circ(A.rec, w);
+      c.d0 = ci.cx; c.d1 = ci.cy; c.d2 = ci.rsq;
+    } else {
+      const double2 p = load_pt(A.rec, w);
+      c.d0 = p.x; c.d1 = p.y; c.d2 = 0.0;
+    }
+  }
+  return c;
 }
 
 // Edge {v, w} is decided by the circle of the smaller vertex id, exactly as
 // hrgen queries from v and keeps ids > v (generator.py:182-187).
-template <bool kSampleIds>
-__device__ __forceinline__ bool pair_test(const QFull& f, const Rec& r, int32_t w, int32_t* idw) {
-  int32_t id = kSampleIds ? r.id : w;
-  *idw = id;
+__device__ __forceinline__ bool pair_test(const QFull& f, const Cand& c, int32_t w) {
   if (w == f.pos) return false;
-  if (id < f.idv) return ref_pred(f.px, f.py, r.cx, r.cy, r.rsq);  // pred(w -> v)
-  return ref_pred(r.px, r.py, f.cx, f.cy, f.rsq);                  // pred(v -> w)
+  if (c.lower) return ref_pred(f.px, f.py, c.d0, c.d1, c.d2);  // pred(w -> v)
+  return ref_pred(c.d0, c.d1, f.cx, f.cy, f.rsq);              // pred(v -> w)
 }
 
 // Shard query enumeration: flat index t over the bands' [qstart, qend).
@@ -719,16 +776,15 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
             }
           }
         }
-        Rec r[4];
+        Cand r[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          if (u < nb) r[u] = load_rec(A.rec + wv[u]);
+          if (u < nb) r[u] = load_cand<kSampleIds>(A, f, wv[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (u < nb) {
-            int32_t idw;
-            const bool hit = pair_test<kSampleIds>(f, r[u], wv[u], &idw);
-            out[i + u] = hit ? idw : -1;
+            const bool hit = pair_test(f, r[u], wv[u]);
+            out[i + u] = hit ? r[u].id : -1;
             hits += hit;
           }
         }
@@ -747,7 +803,7 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
       atomicAdd(&s_hits[wb + q], hits);
     }
     __syncwarp();
-    if (active && !heavy) A.deg[kSampleIds ? rec_id(A.rec + v) : v] = fits ? s_hits[tid] : 0;
+    if (active && !heavy) A.deg[kSampleIds ? __ldg(A.rec.ids + v) : v] = fits ? s_hits[tid] : 0;
     __syncwarp();
   }
 #pragma unroll
@@ -807,7 +863,6 @@ __global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
     for (int32_t base = beg; base < end; base += 128) {
       int32_t wv[4];
       bool ok[4];
-      Rec r[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         int32_t i = base + 32 * u + lane;
@@ -823,14 +878,16 @@ __global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
         int32_t sbb = __shfl_sync(FULL, sB, o);
         wv[u] = tt < la ? sa + tt : sbb + (tt - la);
         ok[u] = i < end;
-        if (ok[u]) r[u] = load_rec(A.rec + wv[u]);
       }
+      Cand r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) r[u] = load_cand<kSampleIds>(A, f, wv[u]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        int32_t idw = 0;
-        bool hit = ok[u] && pair_test<kSampleIds>(f, r[u], wv[u], &idw);
+        bool hit = ok[u] && pair_test(f, r[u], wv[u]);
         unsigned bal = __ballot_sync(FULL, hit);
-        if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = idw;
+        if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = r[u].id;
         hits += __popc(bal);
       }
     }
@@ -970,22 +1027,27 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
 
 constexpr int kCompactThreads = 128;
 constexpr int kSmallSlots = 64;                 // rows sorted by one thread
-constexpr int kTileSlots = 32 * kSmallSlots;    // smem slots per warp
+constexpr int kTileHits = 2048;                 // smem hits per warp
 
 // Compaction of light rows.  A warp owns the same 32 consecutive queries as
-// in k_light, whose staging slices are contiguous: rows of <= kSmallSlots
-// slots are loaded coalesced into shared memory, each lane sorts its row with
-// a register network (misses last), and the warp writes the rows out one by
-// one, 32 lanes wide.  Longer rows are queued for k_sort_warp / k_sort_block.
+// in k_light, whose staging slices form one contiguous range of slots.  The
+// warp streams that range once, dropping the misses (ballot), into shared
+// memory, which leaves each row's hits contiguous and in candidate order.
+// With sample-order ids each lane then sorts its row (<= kSmallSlots hits)
+// with a register network -- hrgen's Graph keeps rows sorted by id
+// (graph.py:69-71); longer rows are queued for an in-place sort.  With
+// angular ids candidate order is id order and nothing is sorted.  Rows are
+// written out one at a time, 32 lanes wide.
 template <bool kSampleIds>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
   __shared__ Band sb[kMaxBands];
   __shared__ QMap qm;
-  __shared__ int32_t buf[kCompactThreads / 32][kTileSlots];
+  __shared__ int32_t buf[kCompactThreads / 32][kTileHits];
   load_qmap(A, qm, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   int32_t* sm = buf[threadIdx.x >> 5];
   const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -996,54 +1058,107 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
     const bool light = active && A.heavy_of[v] < 0;
     int32_t ns = 0, len = 0;
-    int64_t dst = 0, src = 0;
+    int64_t dst = 0, src = INT64_MAX;
     if (light) {
-      const int32_t idv = kSampleIds ? rec_id(A.rec + v) : v;
+      const int32_t idv = kSampleIds ? __ldg(A.rec.ids + v) : v;
       dst = rowptr[idv];
       len = (int32_t)(rowptr[idv + 1] - dst);
       ns = A.slots[v];
       src = A.stage_off[v];
     }
-    const bool small = len > 0 && ns <= kSmallSlots;
-    push_job_warp(J, len > 0 && !small, src, dst, ns, len);
-    // pack the small rows' slices into shared memory: lane offsets by scan
-    const int32_t want = small ? ns : 0;
-    int32_t incl = want;
+    int64_t base = src;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) base = min(base, (int64_t)__shfl_xor_sync(FULL, base, o));
+    int32_t hi = len, si = ns;  // inclusive scans of hits and slots
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
+      const int32_t y = __shfl_up_sync(FULL, hi, o), z = __shfl_up_sync(FULL, si, o);
+      if (lane >= o) { hi += y; si += z; }
     }
-    const int32_t excl = incl - want;
-    unsigned todo = __ballot_sync(FULL, small);
-    {
-      unsigned rows = todo;
-      while (rows) {  // copy each small slice (<= 64 slots) with the whole warp
-        const int l = __ffs(rows) - 1;
-        rows &= rows - 1;
-        const int64_t s0 = __shfl_sync(FULL, src, l);
-        const int32_t n0 = __shfl_sync(FULL, ns, l), e0 = __shfl_sync(FULL, excl, l);
-        for (int k = lane; k < n0; k += 32) sm[e0 + k] = __ldg(A.stage + s0 + k);
+    const int32_t Htot = __shfl_sync(FULL, hi, 31), T = __shfl_sync(FULL, si, 31);
+    const int32_t hexcl = hi - len;
+    if (Htot <= kTileHits) {
+      // stream the slots once; hits land at [hexcl_q, hexcl_q + len_q)
+      int32_t put = 0;
+      for (int32_t i0 = 0; i0 < T; i0 += 128) {
+        int32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t i = i0 + 32 * u + lane;
+          x[u] = i < T ? __ldg(A.stage + base + i) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
+          if (x[u] >= 0) sm[put + __popc(bal & lt)] = x[u];
+          put += __popc(bal);
+        }
       }
-    }
-    __syncwarp();
-    const int32_t mx = __reduce_max_sync(FULL, want);
-    if (mx <= 16) {
-      if (small) thread_sort_smem<16>(sm + excl, ns, len);
-    } else if (mx <= 32) {
-      if (small) thread_sort_smem<32>(sm + excl, ns, len);
+      __syncwarp();
+      if (kSampleIds) {
+        const bool small = len > 1 && len <= kSmallSlots;
+        push_job_warp(J, len > kSmallSlots, -1, dst, len, len);
+        const int32_t mx = __reduce_max_sync(FULL, small ? len : 0);
+        if (mx <= 16) {
+          if (small) thread_sort_smem<16>(sm + hexcl, len, len);
+        } else if (mx <= 32) {
+          if (small) thread_sort_smem<32>(sm + hexcl, len, len);
+        } else {
+          if (small) thread_sort_smem<64>(sm + hexcl, len, len);
+        }
+        __syncwarp();
+      }
+      // angular ids with no deferred query in the tile: the tile's rows are one
+      // contiguous CSR range (consecutive ids), so copy it in one sweep
+      const bool contiguous = !kSampleIds && __all_sync(FULL, !active || light);
+      if (contiguous) {
+        const int64_t d0 = __shfl_sync(FULL, dst, 0);
+        for (int32_t k = lane; k < Htot; k += 32) idx[d0 + k] = sm[k];
+      } else {
+        __shared__ int64_t s_dst[kCompactThreads];
+        __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads];
+        const int wb = threadIdx.x - lane;
+        s_dst[threadIdx.x] = dst;
+        s_len[threadIdx.x] = len;
+        s_off[threadIdx.x] = hexcl;
+        __syncwarp();
+        unsigned todo = __ballot_sync(FULL, len > 0);
+        while (todo) {
+          const int l = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int64_t d = s_dst[wb + l];
+          const int32_t n0 = s_len[wb + l], e0 = s_off[wb + l];
+          for (int32_t k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
+        }
+      }
+      __syncwarp();
     } else {
-      if (small) thread_sort_smem<64>(sm + excl, ns, len);
+      // a hub-heavy tile: compact row by row straight into the CSR
+      unsigned todo = __ballot_sync(FULL, len > 0);
+      while (todo) {
+        const int l = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t d = __shfl_sync(FULL, dst, l);
+        const int32_t n0 = __shfl_sync(FULL, ns, l);
+        const int64_t s0 = __shfl_sync(FULL, src, l);
+        int32_t put = 0;
+        for (int32_t k0 = 0; k0 < n0; k0 += 128) {
+          int32_t x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int32_t k = k0 + 32 * u + lane;
+            x[u] = k < n0 ? __ldg(A.stage + s0 + k) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
+            if (x[u] >= 0) idx[d + put + __popc(bal & lt)] = x[u];
+            put += __popc(bal);
+          }
+        }
+      }
+      if (kSampleIds) push_job_warp(J, len > 1, -1, dst, len, len);
     }
-    __syncwarp();
-    while (todo) {
-      const int l = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int64_t d = __shfl_sync(FULL, dst, l);
-      const int32_t n0 = __shfl_sync(FULL, len, l), e0 = __shfl_sync(FULL, excl, l);
-      for (int k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
-    }
-    __syncwarp();
   }
 }
 
@@ -1202,7 +1317,7 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
     }
     const int64_t e = lo;
     const int32_t v = A.heavy_v[e];
-    const int32_t idv = sample_ids ? rec_id(A.rec + v) : v;
+    const int32_t idv = sample_ids ? __ldg(A.rec.ids + v) : v;
     const int64_t c0 = A.chunk_start[e];
     const int64_t d = rowptr[idv] + (chunk_off[c] - chunk_off[c0]);
     const int32_t h = A.chunk_hits[c];
@@ -1231,7 +1346,7 @@ __global__ void k_queue_heavy_rows(QueryArgs A, int64_t H, const int64_t* __rest
   int64_t b = 0;
   int32_t len = 0;
   if (e < H) {
-    const int32_t idv = rec_id(A.rec + A.heavy_v[e]);
+    const int32_t idv = __ldg(A.rec.ids + A.heavy_v[e]);
     b = rowptr[idv];
     len = (int32_t)(rowptr[idv + 1] - b);
   }
