@@ -19,7 +19,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhrgen_b200.so")
+LIB_PATH = os.environ.get("HRGEN_B200_LIB") or os.path.join(HERE, "libhrgen_b200.so")
 
 HRG_OK = 0
 HRG_ERR_PARAMETER_DOMAIN = 1

@@ -76,7 +76,8 @@ struct hrg_context {
   Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
-      chunk_off, huge_b, huge_e, slots, wtab, job_src, job_dst, job_ns, job_len, job_big;
+      chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
+      sub_off, sub_len, sub_cur, chunk_row, wtab, job_src, job_dst, job_ns, job_len, job_big;
   int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad;
@@ -130,7 +131,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->pt.ensure(16 * (size_t)n));
   CUDA_TRY(c->circ.ensure(sizeof(Circ) * (size_t)n));
   CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
-  CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(64));
+  CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(128));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
   CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
   CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
@@ -263,6 +264,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kLargeSmem));
   }
   unsigned gq = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(n, kLightThreads), c->grid_light));
@@ -278,7 +281,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     A.stage = c->stage.as<int32_t>();
     A.stage_cap = c->stage_cap;
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
-    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 64, st));
+    CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
     else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
@@ -333,9 +336,17 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(c->job_ns.ensure(4 * (size_t)jcap));
   CUDA_TRY(c->job_len.ensure(4 * (size_t)jcap));
   CUDA_TRY(c->job_big.ensure(4 * (size_t)jcap));
-  const int64_t huge_cap = nnz / (kBucketMax + 1) + 1;
-  CUDA_TRY(c->huge_b.ensure(8 * (size_t)huge_cap));
-  CUDA_TRY(c->huge_e.ensure(8 * (size_t)huge_cap));
+  CUDA_TRY(c->large_off.ensure(8 * (size_t)jcap));
+  CUDA_TRY(c->large_len.ensure(4 * (size_t)jcap));
+  const int64_t gcap = nnz / (kLargeMax + 1) + 1;          // giant rows
+  const int64_t bcap = nnz / kGiantTarget + gcap + 1;      // their sub-buckets / chunks
+  CUDA_TRY(c->giant_off.ensure(8 * (size_t)gcap));
+  CUDA_TRY(c->giant_len.ensure(4 * (size_t)gcap));
+  CUDA_TRY(c->giant_meta.ensure(4 * 3 * (size_t)gcap));
+  CUDA_TRY(c->sub_off.ensure(8 * (size_t)bcap));
+  CUDA_TRY(c->sub_len.ensure(4 * (size_t)bcap));
+  CUDA_TRY(c->sub_cur.ensure(8 * (size_t)bcap));
+  CUDA_TRY(c->chunk_row.ensure(4 * (size_t)bcap));
   unsigned long long* ctrs = c->counters.as<unsigned long long>();
   SortJobs J;
   J.src = c->job_src.as<int64_t>();
@@ -345,9 +356,17 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   J.n = reinterpret_cast<unsigned*>(ctrs + 4);
   J.nbig = reinterpret_cast<unsigned*>(ctrs + 5);
   J.big = c->job_big.as<int32_t>();
-  J.nhuge = reinterpret_cast<unsigned*>(ctrs + 6);
-  J.huge_b = c->huge_b.as<int64_t>();
-  J.huge_e = c->huge_e.as<int64_t>();
+  unsigned* uctr = reinterpret_cast<unsigned*>(ctrs + 6);  // 4 more 32-bit counters
+  J.large = RowList{c->large_off.as<int64_t>(), c->large_len.as<int32_t>(), uctr};
+  Giant G;
+  G.rows = RowList{c->giant_off.as<int64_t>(), c->giant_len.as<int32_t>(), uctr + 1};
+  G.sub = RowList{c->sub_off.as<int64_t>(), c->sub_len.as<int32_t>(), uctr + 2};
+  G.nchunks = uctr + 3;
+  G.nb = c->giant_meta.as<int32_t>();
+  G.bbase = G.nb + gcap;
+  G.cbase = G.nb + 2 * gcap;
+  G.chunk_row = c->chunk_row.as<int32_t>();
+  G.cur = c->sub_cur.as<unsigned long long>();
   CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
   if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
   else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
@@ -378,25 +397,19 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(cudaGetLastError());
   c->idx_final = idx;
   if (sample_ids) {
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    const int64_t nh = (int64_t)(ctr[6] & 0xffffffffull);
-    if (nh > 0) {
-      // the few hub rows above kBucketMax: segmented sort, then copy back
-      CUDA_TRY(c->idx2.ensure(4 * (size_t)nnz));
-      size_t sb = 0;
-      CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, idx, c->idx2.as<int32_t>(),
-                                                  (int)nnz, (int)nh, c->huge_b.as<int64_t>(),
-                                                  c->huge_e.as<int64_t>(), st));
-      CUDA_TRY(c->temp.ensure(sb));
-      sb = c->temp.bytes;
-      CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(c->temp.p, sb, idx, c->idx2.as<int32_t>(),
-                                                  (int)nnz, (int)nh, c->huge_b.as<int64_t>(),
-                                                  c->huge_e.as<int64_t>(), st));
-      k_copy_segments<<<(unsigned)std::min<int64_t>(nh, 65535), 1024, 0, st>>>(
-          c->idx2.as<int32_t>(), idx, c->huge_b.as<int64_t>(), c->huge_e.as<int64_t>(), nh);
-      launches++;
-    }
+    // long rows: one block each; giant (hub) rows are first split by value
+    // into sub-buckets through the scratch array
+    CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
+    const RowList none{nullptr, nullptr, nullptr};
+    const unsigned sm = (unsigned)c->sm_count;
+    k_sort_large<<<sm, kLargeThreads, kLargeSmem, st>>>(idx, idx, J.large, G.rows);
+    k_giant_plan<<<1, 1024, 0, st>>>(G);
+    k_giant_hist<<<2 * sm, 1024, 0, st>>>(idx, G, n);
+    k_giant_scan<<<sm, 1024, 0, st>>>(G);
+    k_giant_scatter<<<2 * sm, 1024, 0, st>>>(idx, c->idx2.as<int32_t>(), G, n);
+    k_sort_large<<<sm, kLargeThreads, kLargeSmem, st>>>(c->idx2.as<int32_t>(), idx, G.sub, none);
+    launches += 6;
+    CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
   c->nnz = nnz;
@@ -494,8 +507,9 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
                  &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
-                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->huge_b,
-                 &c->huge_e, &c->slots, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
+                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->slots,
+                 &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
+                 &c->chunk_row, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
                  &c->job_len, &c->job_big, &c->bands, &c->dir, &c->dir_total, &c->bad,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
     b->release();

@@ -993,6 +993,20 @@ __device__ __forceinline__ void warp_sort_slots(const int32_t* src, int32_t ns, 
 
 // Sort job: ns slots at src (stage, or the row itself when in place) ->
 // the first len sorted values to dst.
+// A list of rows to sort: [off, off + len) of a source array, sorted into
+// the same range of a destination array (the same array when in place).
+struct RowList {
+  int64_t* off;
+  int32_t* len;
+  unsigned* n;
+};
+
+__device__ __forceinline__ void push_row(const RowList& R, int64_t off, int32_t len) {
+  const unsigned k = atomicAdd(R.n, 1u);
+  R.off[k] = off;
+  R.len[k] = len;
+}
+
 struct SortJobs {
   int64_t* src;    // offset into stage, or -1: sort idx[dst .. dst+len) in place
   int64_t* dst;
@@ -1001,9 +1015,7 @@ struct SortJobs {
   unsigned* n;     // queued jobs
   unsigned* nbig;  // jobs above kWarpSortMax slots, for k_sort_block
   int32_t* big;    // their job indices
-  unsigned* nhuge; // in-place rows above kBucketMax: segmented sort
-  int64_t* huge_b;
-  int64_t* huge_e;
+  RowList large;   // in-place rows above kBucketMax (or skewed): k_sort_large
 };
 
 constexpr int kWarpSortMax = 256;
@@ -1206,6 +1218,7 @@ __global__ void __launch_bounds__(256) k_sort_warp(const int32_t* __restrict__ s
 }
 
 constexpr int kBucketMax = 4096;   // slots a block bucket sort handles
+constexpr int kSkewBucket = 32;    // a bucket this full means non-uniform ids
 constexpr int kBucketThreads = 256;
 constexpr int kPerThread = kBucketMax / kBucketThreads;
 
@@ -1213,25 +1226,22 @@ constexpr int kPerThread = kBucketMax / kBucketThreads;
 // memory.  Ids are i.i.d. uniform over [0, n) (vertex order = draw order), so
 // P/4 value buckets hold ~4 ids each; misses go to a last bucket.  Buckets
 // are then finished by insertion sort.  Jobs above kBucketMax slots (hub rows,
-// in place) are left to a segmented sort.
+// in place), and rows whose ids are far from uniform, go to k_sort_large.
 __global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __restrict__ stage,
                                                                int32_t* __restrict__ idx,
                                                                SortJobs J, int64_t n_ids) {
   __shared__ int32_t out[kBucketMax];
   __shared__ int32_t cnt[kBucketMax / 4 + 2];
   __shared__ int32_t wsum[kBucketThreads / 32];
+  __shared__ int s_skew;
   const unsigned nb = *J.nbig;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
     const int32_t k = J.big[r];
     const int32_t ns = J.ns[k], len = J.len[k];
     const int64_t s0 = J.src[k], d = J.dst[k];
-    if (ns > kBucketMax) {
-      if (tid == 0) {
-        const unsigned h = atomicAdd(J.nhuge, 1u);
-        J.huge_b[h] = d;
-        J.huge_e[h] = d + len;
-      }
+    if (ns > kBucketMax) {  // in place (every long row is), see k_sort_large
+      if (tid == 0) push_row(J.large, d, len);
       continue;
     }
     const int32_t* src = s0 >= 0 ? stage + s0 : idx + d;
@@ -1239,6 +1249,7 @@ __global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __
     while (4 * B < ns) B <<= 1;  // value buckets; bucket B holds the misses
     const float scale = (float)B / (float)n_ids;
     for (int b = tid; b <= B; b += kBucketThreads) cnt[b] = 0;
+    if (tid == 0) s_skew = 0;
     __syncthreads();
     int32_t x[kPerThread];
     int16_t bk[kPerThread];
@@ -1249,10 +1260,30 @@ __global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __
       bk[u] = -1;
       if (i < ns) {
         bk[u] = x[u] < 0 ? (int16_t)B : (int16_t)min((int)((float)x[u] * scale), B - 1);
-        atomicAdd(&cnt[bk[u]], 1);
+        if (atomicAdd(&cnt[bk[u]], 1) == kSkewBucket && x[u] >= 0) s_skew = 1;
       }
     }
     __syncthreads();
+    // ids far from uniform (user coordinates): insertion sort would go
+    // quadratic, so hand the row to k_sort_large's order-robust path
+    if (s_skew) {
+      if (s0 >= 0) {  // staged slots: compact into the row first
+        __syncthreads();
+        if (tid < 32) {
+          const unsigned lt = (1u << tid) - 1u;
+          int32_t put = 0;
+          for (int i0 = 0; i0 < ns; i0 += 32) {
+            const int32_t v = i0 + tid < ns ? src[i0 + tid] : -1;
+            const unsigned bal = __ballot_sync(0xffffffffu, v >= 0);
+            if (v >= 0) idx[d + put + __popc(bal & lt)] = v;
+            put += __popc(bal);
+          }
+        }
+      }
+      if (tid == 0) push_row(J.large, d, len);
+      __syncthreads();
+      continue;
+    }
     // exclusive scan of cnt[0..B] (B + 1 <= 1025 entries, 256 threads)
     {
       const int per = (B + 1 + kBucketThreads - 1) / kBucketThreads;
@@ -1295,6 +1326,327 @@ __global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __
     }
     __syncthreads();
     for (int i = tid; i < len; i += kBucketThreads) idx[d + i] = out[i];
+    __syncthreads();
+  }
+}
+
+// Ascending sort of a[0, n) by the whole block, any n: the bitonic network
+// in its "mirror, then half-cleaners" form, where every comparator puts the
+// minimum at the lower index, so the positions past n act as +inf padding and
+// their comparators are skipped.  O(n log^2 n); the order-robust fallback.
+__device__ void block_bitonic(int32_t* a, int n) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+        int lo, hi;
+        if (j == (k >> 1)) {  // mirror: i <-> k - 1 - i inside each k-block
+          const int r = t & (j - 1);
+          lo = (t - r) * 2 + r;
+          hi = lo - r + k - 1 - r;
+        } else {              // half-cleaner: i <-> i + j
+          const int r = t & (j - 1);
+          lo = (t - r) * 2 + r;
+          hi = lo + j;
+        }
+        if (hi < n) {
+          const int32_t x = a[lo], y = a[hi];
+          if (y < x) { a[lo] = y; a[hi] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+constexpr int kLargeThreads = 1024;
+constexpr int kLargeMax = 32768;            // ids a k_sort_large block holds
+constexpr int kLargeBuckets = kLargeMax / 4;
+constexpr size_t kLargeSmem = sizeof(int32_t) * (kLargeMax + kLargeBuckets + 1);
+
+// Giant rows (above kLargeMax ids): split by value into sub-buckets of about
+// kGiantTarget ids through a scratch array, kGiantChunk ids per block pass.
+struct Giant {
+  RowList rows;     // the giant rows (in place in idx)
+  RowList sub;      // their sub-buckets: scratch -> idx, same offsets
+  int32_t* nb;      // per giant row: sub-bucket count,
+  int32_t* bbase;   //   first sub-bucket,
+  int32_t* cbase;   //   first chunk
+  int32_t* chunk_row;
+  unsigned* nchunks;
+  unsigned long long* cur;  // per sub-bucket: scatter cursor
+};
+constexpr int kGiantTarget = 16384;
+constexpr int kGiantChunk = 16384;
+constexpr int kGiantMaxB = 4096;   // sub-buckets per giant row (smem counters)
+
+__device__ __forceinline__ int giant_nb(int32_t len) {
+  return min(kGiantMaxB, max(1, (len + kGiantTarget - 1) / kGiantTarget));
+}
+
+// Rows of more than kBucketMax ids: one 1024-thread block per row with the row
+// in shared memory.  The value buckets span the row's own [min, max], so ids
+// that are clustered but not uniform still spread; a bucket holding more
+// than kSkewBucket ids switches the row to the block bitonic network.  Rows
+// above kLargeMax ids are queued as giant (G != nullptr), or -- a sub-bucket
+// of a giant row that still exceeds the block, only for far-from-uniform ids
+// -- sorted by the block network in global memory.
+__global__ void __launch_bounds__(kLargeThreads) k_sort_large(const int32_t* src_base,
+                                                              int32_t* dst_base, RowList R,
+                                                              RowList giant) {
+  extern __shared__ int32_t dsm[];
+  int32_t* out = dsm;
+  int32_t* cnt = dsm + kLargeMax;
+  __shared__ int32_t wsum[kLargeThreads / 32];
+  __shared__ int s_min, s_max, s_skew;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned nr = *R.n;
+  for (unsigned r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int64_t off = R.off[r];
+    const int32_t len = R.len[r];
+    const int32_t* src = src_base + off;
+    int32_t* dst = dst_base + off;
+    if (len > kLargeMax) {
+      if (giant.n) {
+        if (tid == 0) push_row(giant, off, len);
+        continue;
+      }
+      if (src != dst)
+        for (int i = tid; i < len; i += kLargeThreads) dst[i] = src[i];
+      __syncthreads();
+      block_bitonic(dst, len);
+      continue;
+    }
+    if (len <= 1) {
+      if (len == 1 && tid == 0) dst[0] = src[0];
+      continue;
+    }
+    if (tid == 0) { s_min = INT32_MAX; s_max = 0; s_skew = 0; }
+    __syncthreads();
+    int32_t mn = INT32_MAX, mx = 0;
+    for (int i = tid; i < len; i += kLargeThreads) {
+      const int32_t x = src[i];
+      out[i] = x;
+      mn = min(mn, x);
+      mx = max(mx, x);
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
+    const int B = max(1, len >> 2);
+    for (int b = tid; b <= B; b += kLargeThreads) cnt[b] = 0;
+    __syncthreads();
+    mn = s_min;
+    const float scale = (float)B / ((float)(s_max - mn) + 1.0f);
+    for (int i = tid; i < len; i += kLargeThreads) {
+      const int b = min((int)((float)(out[i] - mn) * scale), B - 1);
+      if (atomicAdd(&cnt[b], 1) == kSkewBucket) s_skew = 1;
+    }
+    __syncthreads();
+    if (s_skew) {
+      block_bitonic(out, len);
+    } else {
+      // exclusive scan of cnt[0..B)
+      const int per = (B + kLargeThreads - 1) / kLargeThreads;
+      int32_t acc = 0;
+      for (int q = 0; q < per; ++q) {
+        const int b = tid * per + q;
+        if (b < B) acc += cnt[b];
+      }
+      int32_t inc = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      if (warp == 0) {
+        int32_t w = wsum[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += y;
+        }
+        wsum[lane] = wi - w;
+      }
+      __syncthreads();
+      int32_t run = wsum[warp] + inc - acc;
+      for (int q = 0; q < per; ++q) {
+        const int b = tid * per + q;
+        if (b < B) { const int32_t c = cnt[b]; cnt[b] = run; run += c; }
+      }
+      __syncthreads();
+      // scatter back from the source (L2-resident) into buckets
+      for (int i = tid; i < len; i += kLargeThreads) {
+        const int32_t x = src[i];
+        const int b = min((int)((float)(x - mn) * scale), B - 1);
+        out[atomicAdd(&cnt[b], 1)] = x;
+      }
+      __syncthreads();
+      for (int b = tid; b < B; b += kLargeThreads) {
+        const int beg = b == 0 ? 0 : cnt[b - 1], end = cnt[b];
+        for (int i = beg + 1; i < end; ++i) {
+          const int32_t v = out[i];
+          int j = i - 1;
+          while (j >= beg && out[j] > v) { out[j + 1] = out[j]; --j; }
+          out[j + 1] = v;
+        }
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < len; i += kLargeThreads) dst[i] = out[i];
+    __syncthreads();
+  }
+}
+
+// Giant rows, step 1 (one block): sub-bucket and chunk layout per row, the
+// sub-bucket list (offsets are filled by k_giant_scan), zeroed counters.
+__global__ void __launch_bounds__(1024) k_giant_plan(Giant G) {
+  __shared__ int32_t wb[32], wc[32];
+  __shared__ int32_t s_b, s_c;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned ng = *G.rows.n;
+  if (tid == 0) { s_b = 0; s_c = 0; }
+  __syncthreads();
+  for (unsigned g0 = 0; g0 < ng; g0 += 1024) {
+    const unsigned g = g0 + tid;
+    const int32_t len = g < ng ? G.rows.len[g] : 0;
+    const int32_t nb = g < ng ? giant_nb(len) : 0;
+    const int32_t nc = g < ng ? (len + kGiantChunk - 1) / kGiantChunk : 0;
+    int32_t ib = nb, ic = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, ib, o), z = __shfl_up_sync(0xffffffffu, ic, o);
+      if (lane >= o) { ib += y; ic += z; }
+    }
+    if (lane == 31) { wb[warp] = ib; wc[warp] = ic; }
+    __syncthreads();
+    if (warp == 0) {
+      int32_t a = wb[lane], c = wc[lane], ia = a, icc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, ia, o), z = __shfl_up_sync(0xffffffffu, icc, o);
+        if (lane >= o) { ia += y; icc += z; }
+      }
+      wb[lane] = ia - a;
+      wc[lane] = icc - c;
+    }
+    __syncthreads();
+    const int32_t b0 = s_b + wb[warp] + ib - nb, c0 = s_c + wc[warp] + ic - nc;
+    if (g < ng) {
+      G.nb[g] = nb;
+      G.bbase[g] = b0;
+      G.cbase[g] = c0;
+      for (int32_t q = 0; q < nc; ++q) G.chunk_row[c0 + q] = (int32_t)g;
+      for (int32_t q = 0; q < nb; ++q) G.cur[b0 + q] = 0;
+    }
+    __syncthreads();
+    if (tid == 1023) { s_b = b0 + nb; s_c = c0 + nc; }
+    __syncthreads();
+  }
+  if (tid == 0) { *G.sub.n = (unsigned)s_b; *G.nchunks = (unsigned)s_c; }
+}
+
+__device__ __forceinline__ int giant_bucket(int32_t x, float scale, int nb) {
+  return min((int)((float)x * scale), nb - 1);
+}
+
+// Giant rows, step 2: per-chunk histograms into the sub-bucket counters.
+__global__ void __launch_bounds__(1024) k_giant_hist(const int32_t* __restrict__ idx, Giant G,
+                                                     int64_t n_ids) {
+  __shared__ int32_t h[kGiantMaxB];
+  const unsigned nc = *G.nchunks;
+  for (unsigned c = blockIdx.x; c < nc; c += gridDim.x) {
+    const int32_t g = G.chunk_row[c];
+    const int nb = G.nb[g];
+    const float scale = (float)nb / (float)n_ids;
+    const int64_t off = G.rows.off[g] + (int64_t)(c - G.cbase[g]) * kGiantChunk;
+    const int32_t m = min(kGiantChunk, (int32_t)(G.rows.off[g] + G.rows.len[g] - off));
+    for (int b = threadIdx.x; b < nb; b += 1024) h[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += 1024) atomicAdd(&h[giant_bucket(idx[off + i], scale, nb)], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += 1024)
+      if (h[b]) atomicAdd(G.cur + G.bbase[g] + b, (unsigned long long)h[b]);
+    __syncthreads();
+  }
+}
+
+// Giant rows, step 3: counts -> sub-bucket ranges (absolute offsets) and
+// scatter cursors; one block per giant row.
+__global__ void __launch_bounds__(1024) k_giant_scan(Giant G) {
+  __shared__ int64_t s_run;
+  const unsigned ng = *G.rows.n;
+  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ int64_t ws[32];
+  for (unsigned g = blockIdx.x; g < ng; g += gridDim.x) {
+    const int nb = G.nb[g], b0 = G.bbase[g];
+    if (tid == 0) s_run = G.rows.off[g];
+    __syncthreads();
+    for (int q0 = 0; q0 < nb; q0 += 1024) {
+      const int q = q0 + tid;
+      const int64_t c = q < nb ? (int64_t)G.cur[b0 + q] : 0;
+      int64_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) ws[tid >> 5] = inc;
+      __syncthreads();
+      if (tid < 32) {
+        int64_t w = ws[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += y;
+        }
+        ws[lane] = wi - w;
+      }
+      __syncthreads();
+      const int64_t start = s_run + ws[tid >> 5] + inc - c;
+      if (q < nb) {
+        G.cur[b0 + q] = (unsigned long long)start;
+        G.sub.off[b0 + q] = start;
+        G.sub.len[b0 + q] = (int32_t)c;
+      }
+      __syncthreads();
+      if (tid == 1023) s_run = start + c;
+      __syncthreads();
+    }
+  }
+}
+
+// Giant rows, step 4: scatter each chunk into its sub-buckets of the scratch
+// array (order inside a sub-bucket is fixed by k_sort_large).
+__global__ void __launch_bounds__(1024) k_giant_scatter(const int32_t* __restrict__ idx,
+                                                        int32_t* __restrict__ scratch, Giant G,
+                                                        int64_t n_ids) {
+  __shared__ int32_t h[kGiantMaxB];
+  __shared__ int32_t base[kGiantMaxB];  // relative to the row's offset
+  const unsigned nc = *G.nchunks;
+  for (unsigned c = blockIdx.x; c < nc; c += gridDim.x) {
+    const int32_t g = G.chunk_row[c];
+    const int nb = G.nb[g];
+    const float scale = (float)nb / (float)n_ids;
+    const int64_t off = G.rows.off[g] + (int64_t)(c - G.cbase[g]) * kGiantChunk;
+    const int32_t m = min(kGiantChunk, (int32_t)(G.rows.off[g] + G.rows.len[g] - off));
+    for (int b = threadIdx.x; b < nb; b += 1024) h[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += 1024) atomicAdd(&h[giant_bucket(idx[off + i], scale, nb)], 1);
+    __syncthreads();
+    const int64_t row0 = G.rows.off[g];
+    for (int b = threadIdx.x; b < nb; b += 1024)
+      base[b] = h[b] ? (int32_t)((int64_t)atomicAdd(G.cur + G.bbase[g] + b,
+                                                    (unsigned long long)h[b]) - row0)
+                     : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += 1024) {
+      const int32_t x = idx[off + i];
+      scratch[row0 + atomicAdd(&base[giant_bucket(x, scale, nb)], 1)] = x;
+    }
     __syncthreads();
   }
 }
@@ -1351,29 +1703,6 @@ __global__ void k_queue_heavy_rows(QueryArgs A, int64_t H, const int64_t* __rest
     len = (int32_t)(rowptr[idv + 1] - b);
   }
   push_job_warp(J, len > 1, -1, b, len, len);
-}
-
-__global__ void __launch_bounds__(1024) k_copy_segments(const int32_t* __restrict__ from,
-                                                        int32_t* __restrict__ to,
-                                                        const int64_t* __restrict__ b,
-                                                        const int64_t* __restrict__ e,
-                                                        int64_t H) {
-  for (int64_t s = blockIdx.x; s < H; s += gridDim.x) {
-    const int64_t lo = b[s], hi = e[s];
-    for (int64_t k0 = lo; k0 < hi; k0 += 8 * 1024) {
-      int32_t x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t k = k0 + u * 1024 + threadIdx.x;
-        x[u] = k < hi ? from[k] : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t k = k0 + u * 1024 + threadIdx.x;
-        if (k < hi) to[k] = x[u];
-      }
-    }
-  }
 }
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,

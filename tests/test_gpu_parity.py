@@ -295,3 +295,34 @@ def test_device_csr_tensors():
     assert ip.is_cuda and ix.dtype == torch.int32
     assert np.array_equal(ip.cpu().numpy(), g.indptr)
     assert np.array_equal(ix.cpu().numpy().astype(np.int64), g.indices)
+
+
+@pytest.mark.parametrize("order", ["angle", "shuffled", "blocks"])
+def test_hub_rows_any_id_order(oracle, order):
+    """Rows far above one block's capacity (hubs near the origin) with ids in
+    angular order (clustered, non-uniform in every row), shuffled (uniform)
+    and in interleaved angular blocks: the long-row sorts (block bucket sort,
+    giant-row split, bitonic fallback) must give hrgen's sorted rows."""
+    rng = np.random.default_rng(11)
+    n, R, alpha = 120_000, 14.0, 0.55
+    max_r = P.to_poincare_radius(R)
+    u = rng.random(n)
+    r = np.arccosh(1 + (np.cosh(alpha * R) - 1) * u) / alpha
+    rp = np.minimum(np.tanh(r / 2), np.nextafter(max_r, 0))
+    phi = rng.random(n) * 2 * math.pi
+    rp[:6] = [0.0, 0.01, 0.05, 0.2, 0.4, 0.6]  # hubs
+    if order == "angle":
+        perm = np.argsort(phi, kind="stable")
+    elif order == "shuffled":
+        perm = rng.permutation(n)
+    else:
+        perm = np.argsort(phi, kind="stable").reshape(-1, 1000)[rng.permutation(n // 1000)].ravel()
+    phi, rp = phi[perm], rp[perm]
+    coords = VertexCoordinates(phi=phi, r_native=None, r_poincare=rp)
+    g = P.edges_from_coordinates(coords, R)
+    check_csr(g)
+    assert np.diff(g.indptr).max() > 40_000
+    a = P.model_constants(R, alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(phi, rp, a, alpha, max_r, 512, oracle.TRIG_CR)
+    assert g.m == m
+    assert edge_set_hash(oracle, g) == oracle.edge_hash(e)
