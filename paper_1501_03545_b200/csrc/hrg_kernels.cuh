@@ -27,6 +27,20 @@
 
 namespace hrg {
 
+// tuning knobs (-D overrides for experiments)
+#ifndef HRG_WALK_UNROLL
+#define HRG_WALK_UNROLL 2
+#endif
+#ifndef HRG_BAND_GROUP
+#define HRG_BAND_GROUP 1
+#endif
+#ifndef HRG_SEGCAP
+#define HRG_SEGCAP 24
+#endif
+#ifndef HRG_LIGHT_MINBLOCKS
+#define HRG_LIGHT_MINBLOCKS 6
+#endif
+
 constexpr int kMaxBands = 32;     // one warp lane per radial band
 constexpr int kQBits = 53;
 constexpr uint64_t kQMask = (1ull << kQBits) - 1;
@@ -296,7 +310,7 @@ __global__ void k_dir_tail(const uint64_t* __restrict__ keys, const Band* __rest
 }
 
 constexpr int kLightMax = 2048;    // queries with more candidates take the heavy path
-constexpr int kSegCap = 24;        // non-empty band segments a light query may hold
+constexpr int kSegCap = HRG_SEGCAP;  // non-empty band segments a light query may hold
 constexpr int kChunk = 2048;       // heavy-path work item: candidates of one query
 constexpr int kLightThreads = 128;
 constexpr float kRowStep = 1.0f / 16.0f;  // window table: query-radius row height
@@ -586,7 +600,7 @@ __device__ __forceinline__ void finish_trim(const uint64_t* keys, RawWin& r, uin
   if (r.sB < r.eB && (kB0 & kQMask) < r.tlB) { ++r.sB; trim_lo(keys, r.sB, r.eB, r.tlB); }
 }
 
-constexpr int kBandGroup = 2;
+constexpr int kBandGroup = HRG_BAND_GROUP;
 constexpr int kUnionSmall = 8;     // union windows this small are shared by the tile      // bands resolved together (loads in flight)
 
 // Light pass.  A warp takes 32 consecutive queries (lane = query): each lane
@@ -597,15 +611,63 @@ constexpr int kUnionSmall = 8;     // union windows this small are shared by the
 // slot base + excl(q) + k and receives the neighbour id on a hit, -1
 // otherwise, so every lane does the same amount of work and the row order is
 // the candidate order whoever tests it.  Candidates are fetched 4 at a time.
+// Walk-step candidate data, loaded before the query's side is known in
+// sample order (the full record), or by the query's position in angular
+// order (the circle of a smaller id, else the point).
+struct LoadedCand {
+  double2 a, b;
+  double2 x;  // sample order: (rsq, id bits); angular: unused
+};
+
+template <bool kSampleIds>
+__device__ __forceinline__ LoadedCand load_walk_cand(const QueryArgs& A, int32_t qpos, int32_t w) {
+  LoadedCand c;
+  if (kSampleIds) {
+    load_rec(A.rec, w, c.a, c.b, c.x);
+  } else if (w < qpos) {
+    const double2* q = reinterpret_cast<const double2*>(A.rec.circ + w);
+    c.a = __ldg(q); c.b = __ldg(q + 1);
+  } else {
+    c.a = __ldg(A.rec.pt + w);
+  }
+  return c;
+}
+
+template <bool kSampleIds>
+__device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, int32_t w,
+                                          int32_t& id) {
+  if (kSampleIds) {
+    id = (int32_t)(__double_as_longlong(c.x.y) & 0xffffffffll);
+    if (id == f.idv) return false;
+    if (id < f.idv) return ref_pred(f.px, f.py, c.b.x, c.b.y, c.x.x);  // pred(w -> v)
+    return ref_pred(c.a.x, c.a.y, f.cx, f.cy, f.rsq);                   // pred(v -> w)
+  } else {
+    id = w;
+    if (w == f.pos) return false;
+    if (w < f.pos) return ref_pred(f.px, f.py, c.a.x, c.a.y, c.b.x);
+    return ref_pred(c.a.x, c.a.y, f.cx, f.cy, f.rsq);
+  }
+}
+
+constexpr int kWalkUnroll = HRG_WALK_UNROLL;  // walk steps whose loads are in flight together
+constexpr int kSegStride = kSegCap + 1;
+constexpr int kFirstSeg = 1 << 30;            // flat entry: the query's first segment
+constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | lane  // per-lane segment slots, padded against bank conflicts
+
+struct LightSmem {
+  int2 flat[kLightThreads / 32][32 * kSegStride];  // per warp: the tile's band segments
+  QFull q[kLightThreads];
+  int32_t hits[kLightThreads];
+};
+
 // Queries with more than kLightMax candidates or kSegCap segments are
 // deferred to k_heavy.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
+__global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(QueryArgs A) {
   __shared__ Band sb[kMaxBands];
   __shared__ QMap qm;
-  __shared__ int2 segs[kSegCap][kLightThreads];
-  __shared__ int32_t s_c[kLightThreads], s_n[kLightThreads], s_v[kLightThreads];
-  __shared__ int32_t s_hits[kLightThreads];
+  extern __shared__ __align__(16) unsigned char light_smem[];
+  LightSmem& sm = *reinterpret_cast<LightSmem*>(light_smem);
   load_qmap(A, qm, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -620,6 +682,7 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
     const bool active = t < total_q;
     const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
     int nseg = 0;
+    int2* fl_own = sm.flat[tid >> 5] + lane * kSegStride;
     int32_t c = 0;
     bool ovf = false;
     const double phi = active ? A.q.phi[v] : 0.0;
@@ -697,11 +760,11 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
             }
           }
           if (r.eA > r.sA) {
-            if (nseg < kSegCap) segs[nseg++][tid] = make_int2(r.sA, r.eA - r.sA); else ovf = true;
+            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sA, c); else ovf = true;
             c += r.eA - r.sA;
           }
           if (r.eB > r.sB) {
-            if (nseg < kSegCap) segs[nseg++][tid] = make_int2(r.sB, r.eB - r.sB); else ovf = true;
+            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sB, c); else ovf = true;
             c += r.eB - r.sB;
           }
         }
@@ -709,22 +772,20 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
     }
     cand_local += (unsigned long long)c;
     const bool heavy = active && (c > kLightMax || ovf);
-    const int32_t want = (active && !heavy) ? c : 0;
-    int32_t incl = want;
+    const bool light = active && !heavy;
+    const int32_t want = light ? c : 0, nsl = light ? nseg : 0;
+    int32_t incl = want, sincl = nsl;  // inclusive scans: candidates, segments
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
+      const int32_t y = __shfl_up_sync(FULL, incl, o), z = __shfl_up_sync(FULL, sincl, o);
+      if (lane >= o) { incl += y; sincl += z; }
     }
-    const int32_t T = __shfl_sync(FULL, incl, 31);
+    const int32_t T = __shfl_sync(FULL, incl, 31), S = __shfl_sync(FULL, sincl, 31);
     const int32_t excl = incl - want;
     unsigned long long base = 0;
     if (lane == 31 && T > 0) base = atomicAdd(A.bump, (unsigned long long)T);
     base = __shfl_sync(FULL, base, 31);
-    s_c[tid] = want;
-    s_n[tid] = nseg;
-    s_v[tid] = v;
-    s_hits[tid] = 0;
+    sm.hits[tid] = 0;
     if (heavy) {
       unsigned long long hoff = atomicAdd(A.bump, (unsigned long long)c);
       unsigned e = atomicAdd(A.heavy_n, 1u);
@@ -740,70 +801,89 @@ __global__ void __launch_bounds__(kLightThreads, 4) k_light(QueryArgs A) {
     }
     const bool fits = (int64_t)base + T <= A.stage_cap;
     if (!fits && lane == 0) atomicOr(A.overflow, 1);
-    __syncwarp();
-    // ---- balanced walk over the warp's flattened candidates
-    const int32_t f0 = (int32_t)(((int64_t)T * lane) >> 5);
-    const int32_t f1 = (int32_t)(((int64_t)T * (lane + 1)) >> 5);
-    int q = 0;  // largest lane with excl <= f0
+    // ---- flatten: lane l's segments sit at fl[l * kSegStride + k] as (first
+    // record, offset in the query).  Pack them, in query order, to fl[0, S)
+    // as (first record, kFirstSeg | flat index of the first candidate << 5 |
+    // lane).  Rounds run over destinations; every entry moves down (dest <=
+    // source), so a round's writes never hit a source still to be read.
+    int2* fl = sm.flat[tid >> 5];
+    if (light) sm.q[tid] = load_query<kSampleIds>(A, v);
+    {
+      const int32_t sb = sincl - nsl;
+      for (int e0 = 0; e0 < S; e0 += 32) {
+        const int e = e0 + lane;
+        int l = 0;  // owner: the last lane with sb <= e
 #pragma unroll
-    for (int st = 16; st > 0; st >>= 1) {
-      int32_t ex = __shfl_sync(FULL, excl, q + st);
-      if (ex <= f0) q += st;
+        for (int st = 16; st > 0; st >>= 1)
+          if (__shfl_sync(FULL, sb, l + st) <= e) l += st;
+        const int k = e - __shfl_sync(FULL, sb, l);
+        const int32_t own_ex = __shfl_sync(FULL, excl, l);
+        int2 g = make_int2(0, 0);
+        if (e < S) g = fl[l * kSegStride + k];
+        __syncwarp();
+        if (e < S) fl[e] = make_int2(g.x, (k == 0 ? kFirstSeg : 0) | ((own_ex + g.y) << 5) | l);
+        __syncwarp();
+      }
     }
-    const int32_t q_excl = __shfl_sync(FULL, excl, q);
-    if (fits && f0 < f1) {
-      int32_t k = f0 - q_excl;  // offset inside query q's candidates
-      int sidx = 0;
-      int2 sg = segs[0][wb + q];
-      while (k >= sg.y) { k -= sg.y; sg = segs[++sidx][wb + q]; }
-      int nq = s_n[wb + q];
-      QFull f = load_query<kSampleIds>(A, s_v[wb + q]);
-      int32_t hits = 0;
+    // ---- walk: lane l takes flat candidate i0 + l, so a warp reads 32
+    // consecutive records of one or a few segments per step.  The segment of
+    // each lane comes from a bit mask of the segment starts inside the step.
+    // Hits are counted as a running prefix over flat indices; a query's
+    // count is the prefix at its end minus the prefix at its start.
+    if (fits) {
       int32_t* out = A.stage + base;
-      int32_t i = f0;
-      while (i < f1) {
-        int32_t wv[4];
-        int nb = 0;
-        bool qdone = false;
+      int s0 = 0;          // segment holding flat index i0
+      int32_t pre = 0;     // hits before i0
+      for (int32_t i0 = 0; i0 < T; i0 += 32 * kWalkUnroll) {
+        int32_t wv[kWalkUnroll];
+        int qv[kWalkUnroll];
+        bool qs[kWalkUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (!qdone && i + nb < f1) {
-            wv[u] = sg.x + k;
-            ++nb;
-            if (++k == sg.y) {
-              k = 0;
-              if (++sidx < nq) sg = segs[sidx][wb + q]; else qdone = true;
-            }
-          }
+        for (int u = 0; u < kWalkUnroll; ++u) {
+          const int32_t ib = i0 + 32 * u;
+          const int sl = s0 + 1 + lane;
+          const int32_t st = sl < S ? ((fl[sl].y & kFlatMask) >> 5) : INT32_MAX;
+          const unsigned rel = (unsigned)(st - ib);
+          const unsigned mask = __reduce_or_sync(FULL, rel < 32u ? 1u << rel : 0u);
+          const int my = s0 + __popc(mask & ((2u << lane) - 1u));
+          s0 += __popc(mask);
+          const int2 e = fl[my];
+          const int32_t off = ib + lane - ((e.y & kFlatMask) >> 5);
+          qv[u] = e.y & 31;
+          qs[u] = off == 0 && (e.y & kFirstSeg);  // first candidate of its query
+          wv[u] = e.x + off;
         }
-        Cand r[4];
+        LoadedCand r[kWalkUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (u < nb) r[u] = load_cand<kSampleIds>(A, f, wv[u]);
+        for (int u = 0; u < kWalkUnroll; ++u)
+          if (i0 + 32 * u + lane < T)
+            r[u] = load_walk_cand<kSampleIds>(A, sm.q[wb + qv[u]].pos, wv[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (u < nb) {
-            const bool hit = pair_test(f, r[u], wv[u]);
-            out[i + u] = hit ? r[u].id : -1;
-            hits += hit;
+        for (int u = 0; u < kWalkUnroll; ++u) {
+          const int32_t i = i0 + 32 * u + lane;
+          bool hit = false;
+          if (i < T) {
+            const QFull& f = sm.q[wb + qv[u]];
+            int32_t id;
+            hit = walk_test<kSampleIds>(f, r[u], wv[u], id);
+            out[i] = hit ? id : -1;
           }
-        }
-        i += nb;
-        if (qdone && i < f1) {
-          atomicAdd(&s_hits[wb + q], hits);
-          hits = 0;
-          do { ++q; } while (s_c[wb + q] == 0);
-          sidx = 0;
-          k = 0;
-          sg = segs[0][wb + q];
-          nq = s_n[wb + q];
-          f = load_query<kSampleIds>(A, s_v[wb + q]);
+          const unsigned hm = __ballot_sync(FULL, hit);
+          if (qs[u] && i < T) sm.hits[wb + qv[u]] = pre + __popc(hm & ((1u << lane) - 1u));
+          pre += __popc(hm);
         }
       }
-      atomicAdd(&s_hits[wb + q], hits);
+      // hits of query q = prefix at the next non-empty query (or the end)
+      // minus the prefix at q
+      __syncwarp();
+      const unsigned ne = __ballot_sync(FULL, want > 0) & ~((2u << lane) - 1u);
+      const int32_t mine = sm.hits[tid];
+      const int32_t end = ne ? sm.hits[wb + __ffs(ne) - 1] : pre;
+      __syncwarp();
+      sm.hits[tid] = want > 0 ? end - mine : 0;
     }
     __syncwarp();
-    if (active && !heavy) A.deg[kSampleIds ? __ldg(A.rec.ids + v) : v] = fits ? s_hits[tid] : 0;
+    if (light) A.deg[kSampleIds ? __ldg(A.rec.ids + v) : v] = fits ? sm.hits[tid] : 0;
     __syncwarp();
   }
 #pragma unroll
