@@ -660,6 +660,8 @@ struct LightSmem {
   int32_t hits[kLightThreads];
 };
 
+__device__ __forceinline__ const QFull& f_of(const LightSmem& sm, int q) { return sm.q[q]; }
+
 // Queries with more than kLightMax candidates or kSegCap segments are
 // deferred to k_heavy.
 template <bool kSampleIds>
@@ -796,8 +798,6 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
       A.slots[v] = c;
     } else if (active) {
       A.heavy_of[v] = -1;
-      A.stage_off[v] = (int64_t)base + excl;
-      A.slots[v] = c;
     }
     const bool fits = (int64_t)base + T <= A.stage_cap;
     if (!fits && lane == 0) atomicOr(A.overflow, 1);
@@ -828,8 +828,9 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
     // ---- walk: lane l takes flat candidate i0 + l, so a warp reads 32
     // consecutive records of one or a few segments per step.  The segment of
     // each lane comes from a bit mask of the segment starts inside the step.
-    // Hits are counted as a running prefix over flat indices; a query's
-    // count is the prefix at its end minus the prefix at its start.
+    // Only hits are written, compacted, so a query's hits are one contiguous
+    // run; the running hit prefix at a query's first and past its last
+    // candidate bound that run.
     if (fits) {
       int32_t* out = A.stage + base;
       int s0 = 0;          // segment holding flat index i0
@@ -862,14 +863,13 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
         for (int u = 0; u < kWalkUnroll; ++u) {
           const int32_t i = i0 + 32 * u + lane;
           bool hit = false;
-          if (i < T) {
-            const QFull& f = sm.q[wb + qv[u]];
-            int32_t id;
-            hit = walk_test<kSampleIds>(f, r[u], wv[u], id);
-            out[i] = hit ? id : -1;
-          }
+          int32_t id = 0;
+          if (i < T) hit = walk_test<kSampleIds>(f_of(sm, wb + qv[u]), r[u], wv[u], id);
+          // hits only, compacted: the tile's rows end up back to back
           const unsigned hm = __ballot_sync(FULL, hit);
-          if (qs[u] && i < T) sm.hits[wb + qv[u]] = pre + __popc(hm & ((1u << lane) - 1u));
+          const int32_t at = pre + __popc(hm & ((1u << lane) - 1u));
+          if (hit) out[at] = id;
+          if (qs[u] && i < T) sm.hits[wb + qv[u]] = at;
           pre += __popc(hm);
         }
       }
@@ -881,6 +881,10 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
       const int32_t end = ne ? sm.hits[wb + __ffs(ne) - 1] : pre;
       __syncwarp();
       sm.hits[tid] = want > 0 ? end - mine : 0;
+      if (light) {  // the row's hits: stage[stage_off, stage_off + slots)
+        A.stage_off[v] = (int64_t)base + (want > 0 ? mine : 0);
+        A.slots[v] = want > 0 ? end - mine : 0;
+      }
     }
     __syncwarp();
     if (light) A.deg[kSampleIds ? __ldg(A.rec.ids + v) : v] = fits ? sm.hits[tid] : 0;
@@ -1120,12 +1124,14 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
 constexpr int kCompactThreads = 128;
 constexpr int kSmallSlots = 64;                 // rows sorted by one thread
 constexpr int kTileHits = 2048;                 // smem hits per warp
+constexpr int kCopyUnroll = 8;                  // loads in flight per lane
 
 // Compaction of light rows.  A warp owns the same 32 consecutive queries as
-// in k_light, whose staging slices form one contiguous range of slots.  The
-// warp streams that range once, dropping the misses (ballot), into shared
-// memory, which leaves each row's hits contiguous and in candidate order.
-// With sample-order ids each lane then sorts its row (<= kSmallSlots hits)
+// in k_light, whose hits k_light left back to back in the staging buffer,
+// row after row in candidate order.  With angular ids and no deferred query
+// in the tile the rows are also consecutive in the CSR: one straight copy.
+// Otherwise the warp copies the range into shared memory; with sample-order
+// ids each lane then sorts its row (<= kSmallSlots hits)
 // with a register network -- hrgen's Graph keeps rows sorted by id
 // (graph.py:69-71); longer rows are queued for an in-place sort.  With
 // angular ids candidate order is id order and nothing is sorted.  Rows are
@@ -1139,7 +1145,6 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
   load_qmap(A, qm, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   int32_t* sm = buf[threadIdx.x >> 5];
   const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1169,21 +1174,37 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     }
     const int32_t Htot = __shfl_sync(FULL, hi, 31), T = __shfl_sync(FULL, si, 31);
     const int32_t hexcl = hi - len;
-    if (Htot <= kTileHits) {
-      // stream the slots once; hits land at [hexcl_q, hexcl_q + len_q)
-      int32_t put = 0;
-      for (int32_t i0 = 0; i0 < T; i0 += 128) {
-        int32_t x[4];
+    if (!kSampleIds && __all_sync(FULL, !active || light)) {
+      // angular ids, every query light: staging range == CSR range
+      const int64_t d0 = __shfl_sync(FULL, dst, 0);
+      for (int32_t i0 = 0; i0 < T; i0 += 32 * kCopyUnroll) {
+        int32_t x[kCopyUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kCopyUnroll; ++u) {
           const int32_t i = i0 + 32 * u + lane;
-          x[u] = i < T ? __ldg(A.stage + base + i) : -1;
+          x[u] = i < T ? __ldg(A.stage + base + i) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
-          if (x[u] >= 0) sm[put + __popc(bal & lt)] = x[u];
-          put += __popc(bal);
+        for (int u = 0; u < kCopyUnroll; ++u) {
+          const int32_t i = i0 + 32 * u + lane;
+          if (i < T) idx[d0 + i] = x[u];
+        }
+      }
+    } else if (Htot <= kTileHits) {
+      // the tile's light rows are back to back in the staging buffer
+      // (k_light writes hits only): one coalesced copy into shared memory,
+      // row q at [hexcl_q, hexcl_q + len_q)
+      for (int32_t i0 = 0; i0 < T; i0 += 32 * kCopyUnroll) {
+        int32_t x[kCopyUnroll];
+#pragma unroll
+        for (int u = 0; u < kCopyUnroll; ++u) {
+          const int32_t i = i0 + 32 * u + lane;
+          x[u] = i < T ? __ldg(A.stage + base + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyUnroll; ++u) {
+          const int32_t i = i0 + 32 * u + lane;
+          if (i < T) sm[i] = x[u];
         }
       }
       __syncwarp();
@@ -1200,13 +1221,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
         }
         __syncwarp();
       }
-      // angular ids with no deferred query in the tile: the tile's rows are one
-      // contiguous CSR range (consecutive ids), so copy it in one sweep
-      const bool contiguous = !kSampleIds && __all_sync(FULL, !active || light);
-      if (contiguous) {
-        const int64_t d0 = __shfl_sync(FULL, dst, 0);
-        for (int32_t k = lane; k < Htot; k += 32) idx[d0 + k] = sm[k];
-      } else {
+      {
         __shared__ int64_t s_dst[kCompactThreads];
         __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads];
         const int wb = threadIdx.x - lane;
@@ -1225,7 +1240,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
       }
       __syncwarp();
     } else {
-      // a hub-heavy tile: compact row by row straight into the CSR
+      // a hub-heavy tile: copy row by row straight into the CSR
       unsigned todo = __ballot_sync(FULL, len > 0);
       while (todo) {
         const int l = __ffs(todo) - 1;
@@ -1233,19 +1248,17 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
         const int64_t d = __shfl_sync(FULL, dst, l);
         const int32_t n0 = __shfl_sync(FULL, ns, l);
         const int64_t s0 = __shfl_sync(FULL, src, l);
-        int32_t put = 0;
-        for (int32_t k0 = 0; k0 < n0; k0 += 128) {
-          int32_t x[4];
+        for (int32_t k0 = 0; k0 < n0; k0 += 32 * kCopyUnroll) {
+          int32_t x[kCopyUnroll];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kCopyUnroll; ++u) {
             const int32_t k = k0 + 32 * u + lane;
-            x[u] = k < n0 ? __ldg(A.stage + s0 + k) : -1;
+            x[u] = k < n0 ? __ldg(A.stage + s0 + k) : 0;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
-            if (x[u] >= 0) idx[d + put + __popc(bal & lt)] = x[u];
-            put += __popc(bal);
+          for (int u = 0; u < kCopyUnroll; ++u) {
+            const int32_t k = k0 + 32 * u + lane;
+            if (k < n0) idx[d + k] = x[u];
           }
         }
       }
