@@ -77,7 +77,7 @@ struct hrg_context {
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
-      sub_off, sub_len, sub_cur, chunk_row, wtab, job_src, job_dst, job_ns, job_len, job_big;
+      sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_src, job_dst, job_ns, job_len, job_big;
   int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad;
@@ -259,6 +259,20 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->cosh_r_minus_1,
                                       std::ldexp(1.0, -45), c->wtab.as<float>());
   int launches = 1;
+
+  // query tiles: 32 consecutive positions of one band, band after band
+  // (interleaving the bands' tiles by angle cuts DRAM reads by 40% but
+  // measured slower: the tiles in flight then mix wide and narrow windows)
+  {
+    const int64_t ntmax = n / 32 + L + 1;
+    CUDA_TRY(c->tk0.ensure(8 * (size_t)ntmax));
+    CUDA_TRY(c->tv0.ensure(8 * (size_t)ntmax));
+    k_tile_keys<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
+        A.bands, L, A.keys, ntmax, c->tk0.as<uint64_t>(), c->tv0.as<uint64_t>());
+    A.tiles = c->tv0.as<uint64_t>();
+    A.ntiles = ntmax;
+    launches += 1;
+  }
 
   if (c->grid_light == 0) {
     CUDA_TRY(cudaFuncSetAttribute(k_light<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -513,7 +527,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
-                 &c->chunk_row, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
+                 &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
                  &c->job_len, &c->job_big, &c->bands, &c->dir, &c->dir_total, &c->bad,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
     b->release();

@@ -343,7 +343,43 @@ struct QueryArgs {
   int32_t* chunk_hits;
   int32_t* deg;              // row length per vertex id
   unsigned long long* cand_total;
+  // query tiles: 32 consecutive positions of one band (start | end << 32;
+  // ~0 = no tile)
+  const uint64_t* tiles;
+  int64_t ntiles;            // entries (an upper bound on the tiles)
 };
+
+// Tile table: every band's query range cut into tiles of 32 positions (the
+// key is the angular key of the tile's first point, for an angular
+// interleave of the bands' tiles; unused -- see hrg_api.cu).
+__global__ void k_tile_keys(const Band* __restrict__ bands, int L, const uint64_t* __restrict__ keys,
+                            int64_t ntmax, uint64_t* __restrict__ tkey,
+                            uint64_t* __restrict__ tval) {
+  __shared__ int64_t pre[kMaxBands + 1];
+  if (threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int j = 0; j < L; ++j) {
+      pre[j] = a;
+      a += max(0, bands[j].qend - bands[j].qstart + 31) / 32;
+    }
+    pre[L] = a;
+  }
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntmax;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (k >= pre[L]) {
+      tkey[k] = (1ull << 54) - 1;  // sorts last
+      tval[k] = ~0ull;
+      continue;
+    }
+    int j = 0;
+    while (j + 1 < L && pre[j + 1] <= k) ++j;
+    const int64_t s = bands[j].qstart + (k - pre[j]) * 32;
+    const int64_t e = min(s + 32, (int64_t)bands[j].qend);
+    tkey[k] = __ldg(keys + s) & kQMask;
+    tval[k] = (uint64_t)s | ((uint64_t)e << 32);
+  }
+}
 
 // drop leading positions whose angular key is below ql / trailing ones above qh
 __device__ __forceinline__ void trim_lo(const uint64_t* keys, int32_t& s, int32_t e, uint64_t ql) {
@@ -530,34 +566,9 @@ __device__ __forceinline__ bool pair_test(const QFull& f, const Cand& c, int32_t
   return ref_pred(c.d0, c.d1, f.cx, f.cy, f.rsq);              // pred(v -> w)
 }
 
-// Shard query enumeration: flat index t over the bands' [qstart, qend).
-struct QMap {
-  int64_t off[kMaxBands + 1];
-  int32_t qs[kMaxBands];
-};
-
-__device__ __forceinline__ void load_qmap(const QueryArgs& A, QMap& m, Band* sb) {
+__device__ __forceinline__ void load_bands(const QueryArgs& A, Band* sb) {
   if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int j = 0; j < A.L; ++j) {
-      m.off[j] = acc;
-      m.qs[j] = sb[j].qstart;
-      acc += sb[j].qend - sb[j].qstart;
-    }
-    m.off[A.L] = acc;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ int32_t qmap_pos(const QMap& m, int L, int64_t t) {
-  int lo = 0, hi = L;  // largest j with off[j] <= t
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (m.off[mid] <= t) lo = mid; else hi = mid;
-  }
-  return m.qs[lo] + (int32_t)(t - m.off[lo]);
 }
 
 // Raw (directory-resolved) window of band B: segments [sA,eA) and [sB,eB)
@@ -667,22 +678,22 @@ __device__ __forceinline__ const QFull& f_of(const LightSmem& sm, int q) { retur
 template <bool kSampleIds>
 __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(QueryArgs A) {
   __shared__ Band sb[kMaxBands];
-  __shared__ QMap qm;
   extern __shared__ __align__(16) unsigned char light_smem[];
   LightSmem& sm = *reinterpret_cast<LightSmem*>(light_smem);
-  load_qmap(A, qm, sb);
+  load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
   const int wb = tid - lane;  // first thread of this warp
-  const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long cand_local = 0;
-  for (int64_t tile = wid * 32; tile < total_q; tile += nw * 32) {
-    const int64_t t = tile + lane;
-    const bool active = t < total_q;
-    const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
+  for (int64_t tk = wid; tk < A.ntiles; tk += nw) {
+    const uint64_t tv = __ldg(A.tiles + tk);
+    if (tv == ~0ull) break;
+    const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
+    const bool active = v0 < (int32_t)(tv >> 32);
+    const int32_t v = active ? v0 : 0;
     int nseg = 0;
     int2* fl_own = sm.flat[tid >> 5] + lane * kSegStride;
     int32_t c = 0;
@@ -1140,19 +1151,19 @@ template <bool kSampleIds>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
   __shared__ Band sb[kMaxBands];
-  __shared__ QMap qm;
   __shared__ int32_t buf[kCompactThreads / 32][kTileHits];
-  load_qmap(A, qm, sb);
+  load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   int32_t* sm = buf[threadIdx.x >> 5];
-  const int64_t total_q = qm.off[A.L];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t tile = wid * 32; tile < total_q; tile += nw * 32) {
-    const int64_t t = tile + lane;
-    const bool active = t < total_q;
-    const int32_t v = active ? qmap_pos(qm, A.L, t) : 0;
+  for (int64_t tk = wid; tk < A.ntiles; tk += nw) {
+    const uint64_t tv = __ldg(A.tiles + tk);
+    if (tv == ~0ull) break;
+    const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
+    const bool active = v0 < (int32_t)(tv >> 32);
+    const int32_t v = active ? v0 : 0;
     const bool light = active && A.heavy_of[v] < 0;
     int32_t ns = 0, len = 0;
     int64_t dst = 0, src = INT64_MAX;
