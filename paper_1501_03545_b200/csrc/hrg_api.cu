@@ -77,7 +77,7 @@ struct hrg_context {
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
-      sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_src, job_dst, job_ns, job_len, job_big;
+      sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_dst, job_len, mid_off, mid_len;
   int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad;
@@ -282,8 +282,14 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads, sizeof(LightSmem));
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
-    CUDA_TRY(cudaFuncSetAttribute(k_sort_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kLargeSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kSortWarpSmem));
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<256, kBucketMax, 1>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sort_rows_smem<kBucketMax, 1>()));
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<1024, kLargeMax, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sort_rows_smem<kLargeMax, 2>()));
   }
   unsigned gq = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(n, kLightThreads), c->grid_light));
@@ -347,15 +353,16 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
   int32_t* idx = c->idx.as<int32_t>();
   const int64_t* rp = c->rowptr.as<int64_t>();
-  // sort jobs: light rows of more than 32 slots and (sample order) heavy rows
+  // sort jobs (sample order): light rows above kSmallSlots ids, heavy rows
   const int64_t jcap = n + H + 1;
-  CUDA_TRY(c->job_src.ensure(8 * (size_t)jcap));
+  const int64_t mcap = nnz / (kWarpBucketMax + 1) + 1;
+  const int64_t lcap = nnz / (kBucketMax + 1) + 1;
   CUDA_TRY(c->job_dst.ensure(8 * (size_t)jcap));
-  CUDA_TRY(c->job_ns.ensure(4 * (size_t)jcap));
   CUDA_TRY(c->job_len.ensure(4 * (size_t)jcap));
-  CUDA_TRY(c->job_big.ensure(4 * (size_t)jcap));
-  CUDA_TRY(c->large_off.ensure(8 * (size_t)jcap));
-  CUDA_TRY(c->large_len.ensure(4 * (size_t)jcap));
+  CUDA_TRY(c->mid_off.ensure(8 * (size_t)mcap));
+  CUDA_TRY(c->mid_len.ensure(4 * (size_t)mcap));
+  CUDA_TRY(c->large_off.ensure(8 * (size_t)lcap));
+  CUDA_TRY(c->large_len.ensure(4 * (size_t)lcap));
   const int64_t gcap = nnz / (kLargeMax + 1) + 1;          // giant rows
   const int64_t bcap = nnz / kGiantTarget + gcap + 1;      // their sub-buckets / chunks
   CUDA_TRY(c->giant_off.ensure(8 * (size_t)gcap));
@@ -367,13 +374,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(c->chunk_row.ensure(4 * (size_t)bcap));
   unsigned long long* ctrs = c->counters.as<unsigned long long>();
   SortJobs J;
-  J.src = c->job_src.as<int64_t>();
-  J.dst = c->job_dst.as<int64_t>();
-  J.ns = c->job_ns.as<int32_t>();
-  J.len = c->job_len.as<int32_t>();
-  J.n = reinterpret_cast<unsigned*>(ctrs + 4);
-  J.nbig = reinterpret_cast<unsigned*>(ctrs + 5);
-  J.big = c->job_big.as<int32_t>();
+  J.rows = RowList{c->job_dst.as<int64_t>(), c->job_len.as<int32_t>(),
+                   reinterpret_cast<unsigned*>(ctrs + 4)};
+  J.mid = RowList{c->mid_off.as<int64_t>(), c->mid_len.as<int32_t>(),
+                  reinterpret_cast<unsigned*>(ctrs + 5)};
   unsigned* uctr = reinterpret_cast<unsigned*>(ctrs + 6);  // 4 more 32-bit counters
   J.large = RowList{c->large_off.as<int64_t>(), c->large_len.as<int32_t>(), uctr};
   Giant G;
@@ -404,29 +408,26 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     }
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
-  if (sample_ids) {
-    k_sort_warp<true><<<8 * c->sm_count, 256, 0, st>>>(c->stage.as<int32_t>(), idx, J);
-    k_sort_block<<<8 * c->sm_count, kBucketThreads, 0, st>>>(c->stage.as<int32_t>(), idx, J, n);
-    launches += 2;
-  } else {
-    k_sort_warp<false><<<8 * c->sm_count, 256, 0, st>>>(c->stage.as<int32_t>(), idx, J);
-    launches += 1;
-  }
-  CUDA_TRY(cudaGetLastError());
   c->idx_final = idx;
   if (sample_ids) {
-    // long rows: one block each; giant (hub) rows are first split by value
-    // into sub-buckets through the scratch array
+    // rows by length: a warp (<= kWarpBucketMax), a 256-thread block
+    // (<= kBucketMax), a 1024-thread block (<= kLargeMax); giant (hub) rows
+    // are first split by value into sub-buckets through the scratch array
     CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
     const RowList none{nullptr, nullptr, nullptr};
     const unsigned sm = (unsigned)c->sm_count;
-    k_sort_large<<<sm, kLargeThreads, kLargeSmem, st>>>(idx, idx, J.large, G.rows);
+    k_sort_warp<<<8 * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
+    k_sort_rows<256, kBucketMax, 1><<<8 * sm, 256, sort_rows_smem<kBucketMax, 1>(), st>>>(
+        idx, idx, J.mid, J.large);
+    k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+        idx, idx, J.large, G.rows);
     k_giant_plan<<<1, 1024, 0, st>>>(G);
     k_giant_hist<<<2 * sm, 1024, 0, st>>>(idx, G, n);
     k_giant_scan<<<sm, 1024, 0, st>>>(G);
     k_giant_scatter<<<2 * sm, 1024, 0, st>>>(idx, c->idx2.as<int32_t>(), G, n);
-    k_sort_large<<<sm, kLargeThreads, kLargeSmem, st>>>(c->idx2.as<int32_t>(), idx, G.sub, none);
-    launches += 6;
+    k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+        c->idx2.as<int32_t>(), idx, G.sub, none);
+    launches += 8;
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
@@ -527,8 +528,8 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
-                 &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_src, &c->job_dst, &c->job_ns,
-                 &c->job_len, &c->job_big, &c->bands, &c->dir, &c->dir_total, &c->bad,
+                 &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
+                 &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);

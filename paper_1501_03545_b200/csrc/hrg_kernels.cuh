@@ -1086,8 +1086,6 @@ __device__ __forceinline__ void warp_sort_slots(const int32_t* src, int32_t ns, 
   }
 }
 
-// Sort job: ns slots at src (stage, or the row itself when in place) ->
-// the first len sorted values to dst.
 // A list of rows to sort: [off, off + len) of a source array, sorted into
 // the same range of a destination array (the same array when in place).
 struct RowList {
@@ -1102,33 +1100,30 @@ __device__ __forceinline__ void push_row(const RowList& R, int64_t off, int32_t 
   R.len[k] = len;
 }
 
+// Rows queued for an in-place sort of idx[dst, dst + len): every row is
+// contiguous by then (k_light compacts light rows, heavy rows are compacted
+// chunk by chunk), so a job is just its range.
 struct SortJobs {
-  int64_t* src;    // offset into stage, or -1: sort idx[dst .. dst+len) in place
-  int64_t* dst;
-  int32_t* ns;
-  int32_t* len;
-  unsigned* n;     // queued jobs
-  unsigned* nbig;  // jobs above kWarpSortMax slots, for k_sort_block
-  int32_t* big;    // their job indices
-  RowList large;   // in-place rows above kBucketMax (or skewed): k_sort_large
+  RowList rows;    // queued rows, for k_sort_warp
+  RowList mid;     // rows above kWarpBucketMax: k_sort_rows<256, kBucketMax>
+  RowList large;   // rows above kBucketMax: k_sort_rows<1024, kLargeMax>
 };
 
-constexpr int kWarpSortMax = 256;
-
-// Queue a sort job; called by every lane of a warp (want = this lane has a
-// job), one atomic per warp.
-__device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int64_t src,
-                                              int64_t dst, int32_t ns, int32_t len) {
+// Queue a row; called by every lane of a warp (want = this lane has a row),
+// one atomic per warp.
+__device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int64_t dst,
+                                              int32_t len) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const unsigned bal = __ballot_sync(FULL, want);
   if (!bal) return;
   unsigned base = 0;
-  if (lane == __ffs(bal) - 1) base = atomicAdd(J.n, (unsigned)__popc(bal));
+  if (lane == __ffs(bal) - 1) base = atomicAdd(J.rows.n, (unsigned)__popc(bal));
   base = __shfl_sync(FULL, base, __ffs(bal) - 1);
   if (want) {
     const unsigned k = base + __popc(bal & ((1u << lane) - 1u));
-    J.src[k] = src; J.dst[k] = dst; J.ns[k] = ns; J.len[k] = len;
+    J.rows.off[k] = dst;
+    J.rows.len[k] = len;
   }
 }
 
@@ -1221,7 +1216,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
       __syncwarp();
       if (kSampleIds) {
         const bool small = len > 1 && len <= kSmallSlots;
-        push_job_warp(J, len > kSmallSlots, -1, dst, len, len);
+        push_job_warp(J, len > kSmallSlots, dst, len);
         const int32_t mx = __reduce_max_sync(FULL, small ? len : 0);
         if (mx <= 16) {
           if (small) thread_sort_smem<16>(sm + hexcl, len, len);
@@ -1273,201 +1268,234 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
           }
         }
       }
-      if (kSampleIds) push_job_warp(J, len > 1, -1, dst, len, len);
+      if (kSampleIds) push_job_warp(J, len > 1, dst, len);
     }
   }
 }
 
-// Queued rows.  Angular ids (kSorted == false): candidate order is id order,
-// so a row is just its hits in slot order -- an O(P) ballot compaction, any
-// length.  Sample ids: rows of up to kWarpSortMax slots are sorted by one
-// warp in registers; longer ones go to k_sort_block.
-template <bool kSorted>
-__global__ void __launch_bounds__(256) k_sort_warp(const int32_t* __restrict__ stage,
-                                                   int32_t* __restrict__ idx, SortJobs J) {
-  const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const unsigned nj = *J.n;
-  for (int64_t k = warp; k < nj; k += nwarps) {
-    const int64_t s0 = J.src[k], d = J.dst[k];
-    const int32_t ns = J.ns[k], len = J.len[k];
-    const int32_t* src = s0 >= 0 ? stage + s0 : idx + d;
-    int32_t* dst = idx + d;
-    if (!kSorted) {
-      const unsigned lt = (1u << lane) - 1u;
-      int32_t put = 0;
-      for (int32_t k0 = 0; k0 < ns; k0 += 128) {
-        int32_t x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = k0 + 32 * u + lane;
-          x[u] = i < ns ? __ldg(src + i) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned bal = __ballot_sync(FULL, x[u] >= 0);
-          if (x[u] >= 0) dst[put + __popc(bal & lt)] = x[u];
-          put += __popc(bal);
-        }
-      }
-      continue;
-    }
-    if (ns <= 64) warp_sort_slots<2>(src, ns, dst, len, lane);
-    else if (ns <= 128) warp_sort_slots<4>(src, ns, dst, len, lane);
-    else if (ns <= kWarpSortMax) warp_sort_slots<8>(src, ns, dst, len, lane);
-    else if (lane == 0) J.big[atomicAdd(J.nbig, 1u)] = (int32_t)k;  // one per long row
-  }
-}
+constexpr int kSkewBucket = 32;    // a value bucket this full means non-uniform ids
 
-constexpr int kBucketMax = 4096;   // slots a block bucket sort handles
-constexpr int kSkewBucket = 32;    // a bucket this full means non-uniform ids
-constexpr int kBucketThreads = 256;
-constexpr int kPerThread = kBucketMax / kBucketThreads;
-
-// Jobs above kWarpSortMax slots: one block per job, O(P) bucket sort in shared
-// memory.  Ids are i.i.d. uniform over [0, n) (vertex order = draw order), so
-// P/4 value buckets hold ~4 ids each; misses go to a last bucket.  Buckets
-// are then finished by insertion sort.  Jobs above kBucketMax slots (hub rows,
-// in place), and rows whose ids are far from uniform, go to k_sort_large.
-__global__ void __launch_bounds__(kBucketThreads) k_sort_block(const int32_t* __restrict__ stage,
-                                                               int32_t* __restrict__ idx,
-                                                               SortJobs J, int64_t n_ids) {
-  __shared__ int32_t out[kBucketMax];
-  __shared__ int32_t cnt[kBucketMax / 4 + 2];
-  __shared__ int32_t wsum[kBucketThreads / 32];
-  __shared__ int s_skew;
-  const unsigned nb = *J.nbig;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (unsigned r = blockIdx.x; r < nb; r += gridDim.x) {
-    const int32_t k = J.big[r];
-    const int32_t ns = J.ns[k], len = J.len[k];
-    const int64_t s0 = J.src[k], d = J.dst[k];
-    if (ns > kBucketMax) {  // in place (every long row is), see k_sort_large
-      if (tid == 0) push_row(J.large, d, len);
-      continue;
-    }
-    const int32_t* src = s0 >= 0 ? stage + s0 : idx + d;
-    int B = 1;
-    while (4 * B < ns) B <<= 1;  // value buckets; bucket B holds the misses
-    const float scale = (float)B / (float)n_ids;
-    for (int b = tid; b <= B; b += kBucketThreads) cnt[b] = 0;
-    if (tid == 0) s_skew = 0;
-    __syncthreads();
-    int32_t x[kPerThread];
-    int16_t bk[kPerThread];
-#pragma unroll
-    for (int u = 0; u < kPerThread; ++u) {
-      const int i = tid + u * kBucketThreads;
-      x[u] = i < ns ? src[i] : -1;
-      bk[u] = -1;
-      if (i < ns) {
-        bk[u] = x[u] < 0 ? (int16_t)B : (int16_t)min((int)((float)x[u] * scale), B - 1);
-        if (atomicAdd(&cnt[bk[u]], 1) == kSkewBucket && x[u] >= 0) s_skew = 1;
-      }
-    }
-    __syncthreads();
-    // ids far from uniform (user coordinates): insertion sort would go
-    // quadratic, so hand the row to k_sort_large's order-robust path
-    if (s_skew) {
-      if (s0 >= 0) {  // staged slots: compact into the row first
-        __syncthreads();
-        if (tid < 32) {
-          const unsigned lt = (1u << tid) - 1u;
-          int32_t put = 0;
-          for (int i0 = 0; i0 < ns; i0 += 32) {
-            const int32_t v = i0 + tid < ns ? src[i0 + tid] : -1;
-            const unsigned bal = __ballot_sync(0xffffffffu, v >= 0);
-            if (v >= 0) idx[d + put + __popc(bal & lt)] = v;
-            put += __popc(bal);
-          }
-        }
-      }
-      if (tid == 0) push_row(J.large, d, len);
-      __syncthreads();
-      continue;
-    }
-    // exclusive scan of cnt[0..B] (B + 1 <= 1025 entries, 256 threads)
-    {
-      const int per = (B + 1 + kBucketThreads - 1) / kBucketThreads;
-      int32_t acc = 0;
-      for (int q = 0; q < per; ++q) {
-        const int b = tid * per + q;
-        if (b <= B) acc += cnt[b];
-      }
-      int32_t inc = acc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) wsum[warp] = inc;
-      __syncthreads();
-      int32_t woff = 0;
-      for (int w = 0; w < warp; ++w) woff += wsum[w];
-      int32_t run = woff + inc - acc;
-      for (int q = 0; q < per; ++q) {
-        const int b = tid * per + q;
-        if (b <= B) { const int32_t c = cnt[b]; cnt[b] = run; run += c; }
-      }
-    }
-    __syncthreads();
-    // scatter (order inside a bucket is fixed below)
-#pragma unroll
-    for (int u = 0; u < kPerThread; ++u)
-      if (bk[u] >= 0) out[atomicAdd(&cnt[bk[u]], 1)] = x[u];
-    __syncthreads();
-    // cnt[b] is now the end of bucket b; insertion-sort each value bucket
-    for (int b = tid; b < B; b += kBucketThreads) {
-      const int beg = b == 0 ? 0 : cnt[b - 1], end = cnt[b];
-      for (int i = beg + 1; i < end; ++i) {
-        const int32_t v = out[i];
-        int j = i - 1;
-        while (j >= beg && out[j] > v) { out[j + 1] = out[j]; --j; }
-        out[j + 1] = v;
-      }
-    }
-    __syncthreads();
-    for (int i = tid; i < len; i += kBucketThreads) idx[d + i] = out[i];
-    __syncthreads();
-  }
-}
-
-// Ascending sort of a[0, n) by the whole block, any n: the bitonic network
-// in its "mirror, then half-cleaners" form, where every comparator puts the
-// minimum at the lower index, so the positions past n act as +inf padding and
-// their comparators are skipped.  O(n log^2 n); the order-robust fallback.
-__device__ void block_bitonic(int32_t* a, int n) {
+// Ascending sort of a[0, n) by a group of threads (a warp, kGroup = 32, or
+// the block), any n: the bitonic network in its "mirror, then half-cleaners"
+// form, where every comparator puts the minimum at the lower index, so the
+// positions past n act as +inf padding and their comparators are skipped.
+// O(n log^2 n); the order-robust fallback of the bucket sorts below.
+template <int kGroup>
+__device__ void group_bitonic(int32_t* a, int n, int t0) {
   int P = 1;
   while (P < n) P <<= 1;
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
-        int lo, hi;
-        if (j == (k >> 1)) {  // mirror: i <-> k - 1 - i inside each k-block
-          const int r = t & (j - 1);
-          lo = (t - r) * 2 + r;
-          hi = lo - r + k - 1 - r;
-        } else {              // half-cleaner: i <-> i + j
-          const int r = t & (j - 1);
-          lo = (t - r) * 2 + r;
-          hi = lo + j;
-        }
+      for (int t = t0; t < (P >> 1); t += kGroup) {
+        const int r = t & (j - 1);
+        const int lo = (t - r) * 2 + r;
+        const int hi = j == (k >> 1) ? lo - r + k - 1 - r : lo + j;  // mirror : half-cleaner
         if (hi < n) {
           const int32_t x = a[lo], y = a[hi];
           if (y < x) { a[lo] = y; a[hi] = x; }
         }
       }
-      __syncthreads();
+      if (kGroup == 32) __syncwarp(); else __syncthreads();
     }
   }
 }
 
-constexpr int kLargeThreads = 1024;
-constexpr int kLargeMax = 32768;            // ids a k_sort_large block holds
-constexpr int kLargeBuckets = kLargeMax / 4;
-constexpr size_t kLargeSmem = sizeof(int32_t) * (kLargeMax + kLargeBuckets + 1);
+// Bucket sort of one row held in shared memory (in[0, len)) by a group of
+// kGroup threads, written to dst[0, len) (global; may be the row itself).
+// len >> kShift buckets split the row's own [min, max]: for the i.i.d.-uniform
+// sample-order ids that is O(len) -- count, scan, scatter into tmp, then
+// every id finds its final place by ranking itself inside its (small)
+// bucket.  Returns false (nothing written) if a bucket overflows
+// kSkewBucket, i.e. the ids are far from uniform; the caller then sorts with
+// the bitonic network.  cnt holds (len >> kShift) + 1 counters.  Ids in a
+// row are distinct.  Every thread of the group calls it.
+template <int kGroup, int kShift>
+__device__ bool group_bucket_sort(const int32_t* in, int32_t* tmp, int32_t* cnt, int32_t* dst,
+                                  int len, int t0, int32_t mn, int32_t mx, int* s_flag,
+                                  int32_t* s_wsum) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = t0 & 31;
+  const int B = max(1, len >> kShift);
+  for (int b = t0; b < B; b += kGroup) cnt[b] = 0;
+  if (t0 == 0) *s_flag = 0;
+  if (kGroup == 32) __syncwarp(); else __syncthreads();
+  const float scale = (float)B / ((float)(mx - mn) + 1.0f);
+  for (int i = t0; i < len; i += kGroup) {
+    const int b = min((int)((float)(in[i] - mn) * scale), B - 1);
+    if (atomicAdd(&cnt[b], 1) == kSkewBucket) *s_flag = 1;
+  }
+  if (kGroup == 32) __syncwarp(); else __syncthreads();
+  if (*s_flag) return false;
+  // exclusive scan of cnt[0, B): thread t takes counters [t * per, t * per + per)
+  const int per = (B + kGroup - 1) / kGroup;
+  int32_t acc = 0;
+  for (int q = 0; q < per; ++q) {
+    const int b = t0 * per + q;
+    if (b < B) acc += cnt[b];
+  }
+  int32_t inc = acc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  int32_t woff = 0;
+  if (kGroup > 32) {
+    const int warp = t0 >> 5;
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const int32_t w = lane < kGroup / 32 ? s_wsum[lane] : 0;
+      int32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, wi, o);
+        if (lane >= o) wi += y;
+      }
+      if (lane < kGroup / 32) s_wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    woff = s_wsum[warp];
+  }
+  int32_t run = woff + inc - acc;
+  for (int q = 0; q < per; ++q) {
+    const int b = t0 * per + q;
+    if (b < B) { const int32_t c = cnt[b]; cnt[b] = run; run += c; }
+  }
+  if (kGroup == 32) __syncwarp(); else __syncthreads();
+  for (int i = t0; i < len; i += kGroup) {
+    const int32_t x = in[i];
+    const int b = min((int)((float)(x - mn) * scale), B - 1);
+    tmp[atomicAdd(&cnt[b], 1)] = x;
+  }
+  if (kGroup == 32) __syncwarp(); else __syncthreads();
+  // cnt[b] is now the end of bucket b: rank each id inside its bucket
+  for (int i = t0; i < len; i += kGroup) {
+    const int32_t x = tmp[i];
+    const int b = min((int)((float)(x - mn) * scale), B - 1);
+    const int beg = b == 0 ? 0 : cnt[b - 1], end = cnt[b];
+    int r = beg;
+    for (int j = beg; j < end; ++j) r += tmp[j] < x;
+    dst[r] = x;
+  }
+  if (kGroup == 32) __syncwarp(); else __syncthreads();
+  return true;
+}
+
+constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
+constexpr int kSortWarpThreads = 256;
+struct SortWarpSmem {
+  int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[kWarpBucketMax / 2 + 1];
+  int flag;
+};
+constexpr size_t kSortWarpSmem = sizeof(SortWarpSmem) * (kSortWarpThreads / 32);
+
+// Queued rows (sample-order ids), one warp per row: up to 64 ids by a
+// register network, up to kWarpBucketMax by a bucket sort in shared memory;
+// longer rows go on to k_sort_rows.
+__global__ void __launch_bounds__(kSortWarpThreads) k_sort_warp(int32_t* __restrict__ idx,
+                                                                SortJobs J) {
+  extern __shared__ __align__(16) unsigned char sort_smem[];
+  SortWarpSmem& S = reinterpret_cast<SortWarpSmem*>(sort_smem)[threadIdx.x >> 5];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned nj = *J.rows.n;
+  for (int64_t k = warp; k < nj; k += nwarps) {
+    const int64_t d = J.rows.off[k];
+    const int32_t len = J.rows.len[k];
+    int32_t* row = idx + d;
+    if (len <= 64) {
+      warp_sort_slots<2>(row, len, row, len, lane);
+      continue;
+    }
+    if (len > kWarpBucketMax) {
+      if (lane == 0) push_row(J.mid, d, len);
+      continue;
+    }
+    int32_t mn = INT32_MAX, mx = 0;
+    for (int i = lane; i < len; i += 32) {
+      const int32_t x = row[i];
+      S.in[i] = x;
+      mn = min(mn, x);
+      mx = max(mx, x);
+    }
+    mn = __reduce_min_sync(FULL, mn);
+    mx = __reduce_max_sync(FULL, mx);
+    __syncwarp();
+    if (!group_bucket_sort<32, 1>(S.in, S.tmp, S.cnt, row, len, lane, mn, mx, &S.flag,
+                                  nullptr)) {
+      group_bitonic<32>(S.in, len, lane);
+      for (int i = lane; i < len; i += 32) row[i] = S.in[i];
+    }
+    __syncwarp();
+  }
+}
+
+constexpr int kBucketMax = 4096;   // rows a 256-thread block sorts
+constexpr int kLargeMax = 24576;   // rows a 1024-thread block sorts (in + out: 221 KB)
+template <int kCap, int kShift>
+constexpr size_t sort_rows_smem() { return sizeof(int32_t) * (2 * kCap + (kCap >> kShift) + 1); }
+
+// Rows of up to kCap ids, one block of kThreads per row, in shared memory
+// (bucket sort, bitonic fallback).  Rows above kCap are pushed to `over`
+// (when given); without one -- a sub-bucket of a giant row that still
+// exceeds the block, only for far-from-uniform ids -- the block sorts the
+// row by the bitonic network in global memory.
+template <int kThreads, int kCap, int kShift>
+__global__ void __launch_bounds__(kThreads) k_sort_rows(const int32_t* src_base,
+                                                        int32_t* dst_base, RowList R,
+                                                        RowList over) {
+  extern __shared__ __align__(16) unsigned char rows_smem[];
+  int32_t* in = reinterpret_cast<int32_t*>(rows_smem);
+  int32_t* out = in + kCap;
+  int32_t* cnt = out + kCap;  // (kCap >> kShift) + 1
+  __shared__ int32_t s_wsum[32];
+  __shared__ int s_min, s_max, s_flag;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned nr = *R.n;
+  for (unsigned r = blockIdx.x; r < nr; r += gridDim.x) {
+    const int64_t off = R.off[r];
+    const int32_t len = R.len[r];
+    const int32_t* src = src_base + off;
+    int32_t* dst = dst_base + off;
+    if (len > kCap) {
+      if (over.n) {
+        if (tid == 0) push_row(over, off, len);
+        continue;
+      }
+      if (src != dst)
+        for (int i = tid; i < len; i += kThreads) dst[i] = src[i];
+      __syncthreads();
+      group_bitonic<kThreads>(dst, len, tid);
+      continue;
+    }
+    if (len <= 1) {
+      if (len == 1 && tid == 0) dst[0] = src[0];
+      continue;
+    }
+    if (tid == 0) { s_min = INT32_MAX; s_max = 0; }
+    __syncthreads();
+    int32_t mn = INT32_MAX, mx = 0;
+    for (int i = tid; i < len; i += kThreads) {
+      const int32_t x = src[i];
+      in[i] = x;
+      mn = min(mn, x);
+      mx = max(mx, x);
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
+    __syncthreads();
+    if (!group_bucket_sort<kThreads, kShift>(in, out, cnt, dst, len, tid, s_min, s_max, &s_flag,
+                                              s_wsum)) {
+      group_bitonic<kThreads>(in, len, tid);
+      for (int i = tid; i < len; i += kThreads) dst[i] = in[i];
+    }
+    __syncthreads();
+  }
+}
 
 // Giant rows (above kLargeMax ids): split by value into sub-buckets of about
 // kGiantTarget ids through a scratch array, kGiantChunk ids per block pass.
@@ -1487,122 +1515,6 @@ constexpr int kGiantMaxB = 4096;   // sub-buckets per giant row (smem counters)
 
 __device__ __forceinline__ int giant_nb(int32_t len) {
   return min(kGiantMaxB, max(1, (len + kGiantTarget - 1) / kGiantTarget));
-}
-
-// Rows of more than kBucketMax ids: one 1024-thread block per row with the row
-// in shared memory.  The value buckets span the row's own [min, max], so ids
-// that are clustered but not uniform still spread; a bucket holding more
-// than kSkewBucket ids switches the row to the block bitonic network.  Rows
-// above kLargeMax ids are queued as giant (G != nullptr), or -- a sub-bucket
-// of a giant row that still exceeds the block, only for far-from-uniform ids
-// -- sorted by the block network in global memory.
-__global__ void __launch_bounds__(kLargeThreads) k_sort_large(const int32_t* src_base,
-                                                              int32_t* dst_base, RowList R,
-                                                              RowList giant) {
-  extern __shared__ int32_t dsm[];
-  int32_t* out = dsm;
-  int32_t* cnt = dsm + kLargeMax;
-  __shared__ int32_t wsum[kLargeThreads / 32];
-  __shared__ int s_min, s_max, s_skew;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned nr = *R.n;
-  for (unsigned r = blockIdx.x; r < nr; r += gridDim.x) {
-    const int64_t off = R.off[r];
-    const int32_t len = R.len[r];
-    const int32_t* src = src_base + off;
-    int32_t* dst = dst_base + off;
-    if (len > kLargeMax) {
-      if (giant.n) {
-        if (tid == 0) push_row(giant, off, len);
-        continue;
-      }
-      if (src != dst)
-        for (int i = tid; i < len; i += kLargeThreads) dst[i] = src[i];
-      __syncthreads();
-      block_bitonic(dst, len);
-      continue;
-    }
-    if (len <= 1) {
-      if (len == 1 && tid == 0) dst[0] = src[0];
-      continue;
-    }
-    if (tid == 0) { s_min = INT32_MAX; s_max = 0; s_skew = 0; }
-    __syncthreads();
-    int32_t mn = INT32_MAX, mx = 0;
-    for (int i = tid; i < len; i += kLargeThreads) {
-      const int32_t x = src[i];
-      out[i] = x;
-      mn = min(mn, x);
-      mx = max(mx, x);
-    }
-    mn = __reduce_min_sync(0xffffffffu, mn);
-    mx = __reduce_max_sync(0xffffffffu, mx);
-    if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
-    const int B = max(1, len >> 2);
-    for (int b = tid; b <= B; b += kLargeThreads) cnt[b] = 0;
-    __syncthreads();
-    mn = s_min;
-    const float scale = (float)B / ((float)(s_max - mn) + 1.0f);
-    for (int i = tid; i < len; i += kLargeThreads) {
-      const int b = min((int)((float)(out[i] - mn) * scale), B - 1);
-      if (atomicAdd(&cnt[b], 1) == kSkewBucket) s_skew = 1;
-    }
-    __syncthreads();
-    if (s_skew) {
-      block_bitonic(out, len);
-    } else {
-      // exclusive scan of cnt[0..B)
-      const int per = (B + kLargeThreads - 1) / kLargeThreads;
-      int32_t acc = 0;
-      for (int q = 0; q < per; ++q) {
-        const int b = tid * per + q;
-        if (b < B) acc += cnt[b];
-      }
-      int32_t inc = acc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) wsum[warp] = inc;
-      __syncthreads();
-      if (warp == 0) {
-        int32_t w = wsum[lane], wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-          if (lane >= o) wi += y;
-        }
-        wsum[lane] = wi - w;
-      }
-      __syncthreads();
-      int32_t run = wsum[warp] + inc - acc;
-      for (int q = 0; q < per; ++q) {
-        const int b = tid * per + q;
-        if (b < B) { const int32_t c = cnt[b]; cnt[b] = run; run += c; }
-      }
-      __syncthreads();
-      // scatter back from the source (L2-resident) into buckets
-      for (int i = tid; i < len; i += kLargeThreads) {
-        const int32_t x = src[i];
-        const int b = min((int)((float)(x - mn) * scale), B - 1);
-        out[atomicAdd(&cnt[b], 1)] = x;
-      }
-      __syncthreads();
-      for (int b = tid; b < B; b += kLargeThreads) {
-        const int beg = b == 0 ? 0 : cnt[b - 1], end = cnt[b];
-        for (int i = beg + 1; i < end; ++i) {
-          const int32_t v = out[i];
-          int j = i - 1;
-          while (j >= beg && out[j] > v) { out[j + 1] = out[j]; --j; }
-          out[j + 1] = v;
-        }
-      }
-      __syncthreads();
-    }
-    for (int i = tid; i < len; i += kLargeThreads) dst[i] = out[i];
-    __syncthreads();
-  }
 }
 
 // Giant rows, step 1 (one block): sub-bucket and chunk layout per row, the
@@ -1724,7 +1636,7 @@ __global__ void __launch_bounds__(1024) k_giant_scan(Giant G) {
 }
 
 // Giant rows, step 4: scatter each chunk into its sub-buckets of the scratch
-// array (order inside a sub-bucket is fixed by k_sort_large).
+// array (order inside a sub-bucket is fixed by k_sort_rows).
 __global__ void __launch_bounds__(1024) k_giant_scatter(const int32_t* __restrict__ idx,
                                                         int32_t* __restrict__ scratch, Giant G,
                                                         int64_t n_ids) {
@@ -1806,7 +1718,7 @@ __global__ void k_queue_heavy_rows(QueryArgs A, int64_t H, const int64_t* __rest
     b = rowptr[idv];
     len = (int32_t)(rowptr[idv + 1] - b);
   }
-  push_job_warp(J, len > 1, -1, b, len, len);
+  push_job_warp(J, len > 1, b, len);
 }
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,
