@@ -83,7 +83,7 @@ struct hrg_context {
   Buf bands, dir, dir_total, bad;
   // CSR
   Buf deg, rowptr, idx, idx2, cand;
-  Buf temp;
+  Buf temp, k32_in, k32_out;
   Buf widen;
   int64_t n = 0, nnz = 0;
   bool have_result = false;
@@ -155,37 +155,47 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                        const hrg_shard* shard, double C, bool sample_ids) {
   int64_t n = M->n;
   cudaStream_t st = c->stream;
-  int end_bit = kQBits + 6;
+  CUDA_TRY(c->k32_in.ensure(4 * (size_t)n));
+  CUDA_TRY(c->k32_out.ensure(4 * (size_t)n));
+  k_sort_keys32<<<blocks_for(n), 256, 0, st>>>(n, c->keys_in.as<uint64_t>(),
+                                               c->k32_in.as<uint32_t>());
   size_t tb = 0;
-  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->keys_in.as<uint64_t>(),
-                                           c->keys_out.as<uint64_t>(), c->vals_in.as<int32_t>(),
-                                           c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->k32_in.as<uint32_t>(),
+                                           c->k32_out.as<uint32_t>(), c->vals_in.as<int32_t>(),
+                                           c->vals_out.as<int32_t>(), (int)n, 0, 32, st));
   CUDA_TRY(c->temp.ensure(tb));
   tb = c->temp.bytes;
-  CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->temp.p, tb, c->keys_in.as<uint64_t>(),
-                                           c->keys_out.as<uint64_t>(), c->vals_in.as<int32_t>(),
-                                           c->vals_out.as<int32_t>(), (int)n, 0, end_bit, st));
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(c->temp.p, tb, c->k32_in.as<uint32_t>(),
+                                           c->k32_out.as<uint32_t>(), c->vals_in.as<int32_t>(),
+                                           c->vals_out.as<int32_t>(), (int)n, 0, 32, st));
   CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
   QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
   const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
                   c->vals_out.as<int32_t>()};
   if (sample_ids)
-    k_gather<true><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
+    k_gather<true><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(),
+                                                  c->keys_in.as<uint64_t>(),
+                                                  c->keys_out.as<uint64_t>(), c->phi.as<double>(),
                                                   c->rp.as<double>(), c->rn.as<double>(),
                                                   M->cosh_r_minus_1, recs, q,
                                                   c->s_rp.as<double>(), c->s_rn.as<double>());
   else
-    k_gather<false><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(), c->phi.as<double>(),
+    k_gather<false><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(),
+                                                   c->keys_in.as<uint64_t>(),
+                                                   c->keys_out.as<uint64_t>(), c->phi.as<double>(),
                                                    c->rp.as<double>(), c->rn.as<double>(),
                                                    M->cosh_r_minus_1, recs, q,
                                                    c->s_rp.as<double>(), c->s_rn.as<double>());
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
-    uint64_t span = (uint64_t)1 << kQBits;
+    // sector bounds on the sort granularity (multiples of 2^kSortShift)
+    const uint64_t span = (uint64_t)1 << (kQBits - kSortShift);
     qlo = ((uint64_t)shard->index * span + (uint64_t)shard->count - 1) / (uint64_t)shard->count;
     qhi = ((uint64_t)(shard->index + 1) * span + (uint64_t)shard->count - 1) /
           (uint64_t)shard->count;
     if (shard->index + 1 == shard->count) qhi = span;
+    qlo <<= kSortShift;
+    qhi <<= kSortShift;
   }
   k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>());
@@ -530,7 +540,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad,
-                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->widen})
+                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   delete c;

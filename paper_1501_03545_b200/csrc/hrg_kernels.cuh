@@ -159,8 +159,26 @@ struct QRec {          // query-side extras, per sorted position
 // Gather into (band, angle) order and precompute every per-point quantity the
 // query needs.  p_x/p_y: quadtree.py:474-475; c_x/c_y/rad^2: quadtree.py:516-518
 // with center_r/rad from geometry.py:141-157.
+// Sort key: band << 27 | top 27 bits of the angular key.  Points are ordered
+// by (band, angle) to 2^-27 of a turn; ties keep draw order (stable sort).
+// Everything that relies on the order works at that granularity or coarser:
+// directory buckets (shift >= kSortShift), shard sector bounds (multiples of
+// 2^kSortShift) and the exact key trims, which drop a point only on its own
+// full key and so stay correct on any order.
+constexpr int kSortShift = kQBits - 27;
+__global__ void __launch_bounds__(256) k_sort_keys32(int64_t n, const uint64_t* __restrict__ keys,
+                                                     uint32_t* __restrict__ k32) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) {
+    const uint64_t k = keys[i];
+    k32[i] = (uint32_t)((k >> kQBits) << 27) | (uint32_t)((k & kQMask) >> kSortShift);
+  }
+}
+
 template <bool kSampleIds>
 __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __restrict__ perm,
+                                                const uint64_t* __restrict__ keys_in,
+                                                uint64_t* __restrict__ keys_out,
                                                 const double* __restrict__ phi,
                                                 const double* __restrict__ rp,
                                                 const double* __restrict__ rn, double a,
@@ -170,6 +188,7 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __rest
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   int32_t i = perm[p];
+  keys_out[p] = keys_in[i];
   double ph = phi[i], r = rp[i];
   double sn, cs;
   sincos_cr(ph, &sn, &cs);
@@ -224,7 +243,7 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     B.qend = qsec_hi > kQMask ? B.end : (int32_t)lower_bound_u64(keys, n, base | qsec_hi);
     int64_t cnt = B.end - B.start;
     int lg = 0;
-    while ((1ll << lg) < cnt) ++lg;       // nb = next pow2 >= cnt (>= 1)
+    while ((1ll << lg) < cnt && lg < kQBits - kSortShift) ++lg;  // nb = next pow2 >= cnt
     B.nb = 1 << lg;
     B.shift = kQBits - lg;
     B.rmin = __int_as_float(0x7f800000);

@@ -30,12 +30,16 @@ def angular_key(phi):
     return q.astype(np.uint64)
 
 
+SORT_SHIFT = Q_BITS - 27  # the device orders points to 2^-27 of a turn
+
+
 def sector_bounds(index: int, count: int):
-    """Half-open key range [lo, hi) of sector `index` of `count`."""
-    span = 2**Q_BITS
+    """Half-open key range [lo, hi) of sector `index` of `count`: an even
+    split of the 2^27 sort-granularity angles (hrg_api.cu build_index)."""
+    span = 2**(Q_BITS - SORT_SHIFT)
     lo = (index * span + count - 1) // count
     hi = span if index + 1 == count else ((index + 1) * span + count - 1) // count
-    return lo, hi
+    return lo << SORT_SHIFT, hi << SORT_SHIFT
 
 
 def sector_of(phi, count: int):
