@@ -23,6 +23,7 @@
 // and generator.py:190-225.
 #pragma once
 #include <stdint.h>
+#include <utility>
 #include "hrg_math.cuh"
 
 namespace hrg {
@@ -33,6 +34,9 @@ namespace hrg {
 #endif
 #ifndef HRG_BAND_GROUP
 #define HRG_BAND_GROUP 1
+#endif
+#ifndef HRG_SMALL_SLOTS
+#define HRG_SMALL_SLOTS 64
 #endif
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
@@ -1048,6 +1052,41 @@ __device__ __forceinline__ void warp_bitonic(int32_t (&x)[E], int lane) {
   }
 }
 
+// Batcher's odd-even merge sort network over a register array, ascending:
+// 63 / 191 / 543 comparators for 16 / 32 / 64 keys against bitonic's 80 /
+// 240 / 672.  oe_idx enumerates the comparators at compile time; the fold
+// below instantiates each with constant register indices.
+template <int N>
+__host__ __device__ constexpr int oe_idx(int c, bool hi) {
+  int m = 0;
+  for (int p = 1; p < N; p <<= 1)
+    for (int k = p; k >= 1; k >>= 1)
+      for (int j = k % p; j + k < N; j += 2 * k)
+        for (int i = 0; i < k && i + j + k < N; ++i)
+          if ((i + j) / (2 * p) == (i + j + k) / (2 * p)) {
+            if (m == c) return hi ? i + j + k : i + j;
+            ++m;
+          }
+  return m;  // past the last comparator: their count
+}
+
+template <int Lo, int Hi, int N>
+__device__ __forceinline__ void cmpx(int32_t (&x)[N]) {
+  const int32_t a = x[Lo], b = x[Hi];
+  x[Lo] = min(a, b);
+  x[Hi] = max(a, b);
+}
+
+template <int N, int... C>
+__device__ __forceinline__ void oe_apply(int32_t (&x)[N], std::integer_sequence<int, C...>) {
+  (cmpx<oe_idx<N>(C, false), oe_idx<N>(C, true)>(x), ...);
+}
+
+template <int N>
+__device__ __forceinline__ void reg_oddeven(int32_t (&x)[N]) {
+  oe_apply<N>(x, std::make_integer_sequence<int, oe_idx<N>(1 << 30, false)>{});
+}
+
 // Bitonic network over a register array (compile-time indices throughout).
 template <int N>
 __device__ __forceinline__ void reg_bitonic(int32_t (&x)[N]) {
@@ -1081,7 +1120,7 @@ __device__ __forceinline__ void thread_sort_smem(int32_t* sm, int32_t ns, int32_
   int32_t x[N];
 #pragma unroll
   for (int t = 0; t < N; ++t) x[t] = t < ns ? miss_last(sm[t]) : INT32_MAX;
-  reg_bitonic<N>(x);
+  reg_oddeven<N>(x);
 #pragma unroll
   for (int t = 0; t < N; ++t)
     if (t < len) sm[t] = x[t];
@@ -1147,7 +1186,7 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
 }
 
 constexpr int kCompactThreads = 128;
-constexpr int kSmallSlots = 64;                 // rows sorted by one thread
+constexpr int kSmallSlots = HRG_SMALL_SLOTS;    // rows sorted by one thread (32 or 64)
 constexpr int kTileHits = 2048;                 // smem hits per warp
 constexpr int kCopyUnroll = 8;                  // loads in flight per lane
 
@@ -1241,8 +1280,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
           if (small) thread_sort_smem<16>(sm + hexcl, len, len);
         } else if (mx <= 32) {
           if (small) thread_sort_smem<32>(sm + hexcl, len, len);
-        } else {
-          if (small) thread_sort_smem<64>(sm + hexcl, len, len);
+        } else if (kSmallSlots > 32) {
+          if (small) thread_sort_smem<kSmallSlots>(sm + hexcl, len, len);
         }
         __syncwarp();
       }
