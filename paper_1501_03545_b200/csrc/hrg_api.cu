@@ -136,7 +136,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
   CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
-  CUDA_TRY(c->dir.ensure(4 * (size_t)(2 * n + 2 * kMaxBands + 64)));
+  CUDA_TRY(c->dir.ensure(4 * (size_t)((2 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->dir_total.ensure(8)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
   CUDA_TRY(c->deg.ensure(i32)); CUDA_TRY(c->rowptr.ensure(8 * (size_t)(n + 1)));
   return HRG_OK;

@@ -38,6 +38,21 @@ namespace hrg {
 #ifndef HRG_SMALL_SLOTS
 #define HRG_SMALL_SLOTS 64
 #endif
+#ifndef HRG_TRIM
+#define HRG_TRIM 0
+#endif
+#ifndef HRG_TRIM_UNION
+#define HRG_TRIM_UNION 1
+#endif
+#ifndef HRG_DIR_EXTRA
+#define HRG_DIR_EXTRA 1
+#endif
+#ifndef HRG_SHARE_SLACK
+#define HRG_SHARE_SLACK -100000
+#endif
+#ifndef HRG_UNION_SMALL
+#define HRG_UNION_SMALL 2
+#endif
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
 #endif
@@ -170,6 +185,7 @@ struct QRec {          // query-side extras, per sorted position
 // 2^kSortShift) and the exact key trims, which drop a point only on its own
 // full key and so stay correct on any order.
 constexpr int kSortShift = kQBits - 27;
+constexpr int kDirExtra = HRG_DIR_EXTRA;  // directory buckets per point: 1-2 x 2^kDirExtra
 __global__ void __launch_bounds__(256) k_sort_keys32(int64_t n, const uint64_t* __restrict__ keys,
                                                      uint32_t* __restrict__ k32) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -248,6 +264,7 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     int64_t cnt = B.end - B.start;
     int lg = 0;
     while ((1ll << lg) < cnt && lg < kQBits - kSortShift) ++lg;  // nb = next pow2 >= cnt
+    lg = min(lg + kDirExtra, kQBits - kSortShift);                // (x 2^kDirExtra)
     B.nb = 1 << lg;
     B.shift = kQBits - lg;
     B.rmin = __int_as_float(0x7f800000);
@@ -634,17 +651,13 @@ __device__ __forceinline__ void finish_trim(const uint64_t* keys, RawWin& r, uin
   if (r.sB < r.eB && (kB0 & kQMask) < r.tlB) { ++r.sB; trim_lo(keys, r.sB, r.eB, r.tlB); }
 }
 
-constexpr int kBandGroup = HRG_BAND_GROUP;
-constexpr int kUnionSmall = 8;     // union windows this small are shared by the tile      // bands resolved together (loads in flight)
+constexpr int kBandGroup = HRG_BAND_GROUP;    // bands resolved together (loads in flight)
+constexpr bool kTrim = HRG_TRIM;              // exact key trim of per-query windows
+constexpr bool kTrimUnion = HRG_TRIM_UNION;   // ... and of the tile's union windows
+constexpr int kUnionSmall = HRG_UNION_SMALL;  // union windows this small are shared by the tile
+constexpr int kShareSlack = HRG_SHARE_SLACK;  // (experiment) union shared if it exceeds the
+                                              // tile's narrowest window by at most this
 
-// Light pass.  A warp takes 32 consecutive queries (lane = query): each lane
-// resolves its windows in every band (table half-width, directory, exact
-// trim; kBandGroup bands at a time so their loads overlap) into a segment
-// list in shared memory.  The warp then splits the concatenation of all 32
-// candidate lists evenly over its lanes; candidate k of query q owns staging
-// slot base + excl(q) + k and receives the neighbour id on a hit, -1
-// otherwise, so every lane does the same amount of work and the row order is
-// the candidate order whoever tests it.  Candidates are fetched 4 at a time.
 // Walk-step candidate data, loaded before the query's side is known in
 // sample order (the full record), or by the query's position in angular
 // order (the circle of a smaller id, else the point).
@@ -732,12 +745,13 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
     int32_t uA = 0, uAe = 0, uB = 0, uBe = 0;
     {
       double pmin = active ? phi : 1e300, pmax = active ? phi : -1e300;
-      float rmin = rvq;
+      float rmin = rvq, rmax = active ? rvq : 0.0f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         pmin = fmin(pmin, __shfl_xor_sync(FULL, pmin, o));
         pmax = fmax(pmax, __shfl_xor_sync(FULL, pmax, o));
         rmin = fminf(rmin, __shfl_xor_sync(FULL, rmin, o));
+        rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, o));
       }
       if (pmax >= pmin && pmax - pmin < 0.5 && lane < A.L) {
         const float dlt = __ldg(wtab_row(A, rmin) + lane);
@@ -745,14 +759,22 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
         RawWin r = raw_window(A, sb[lane], 0.5 * (pmin + pmax),
                               (dlt < 0.0f || dlt >= 3.14159265f)
                                   ? dlt : __double2float_ru((double)dlt + half));
-        const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
-        const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
-        const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
-        finish_trim(A.keys, r, kA0, kA1, kB0);
+        if (kTrimUnion) {
+          const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
+          const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
+          const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
+          finish_trim(A.keys, r, kA0, kA1, kB0);
+        }
         if (r.sB < r.eB && r.sB < r.eA) { r.sA = sb[lane].start; r.eA = sb[lane].end; r.sB = r.eB = 0; }
         uA = r.sA; uAe = r.eA; uB = r.sB; uBe = r.eB;
         const int32_t un = (uAe - uA) + (uBe - uB);
-        if (un <= kUnionSmall) cheap = 1;
+        // the narrowest window of the tile (its outermost query), in points:
+        // if the union exceeds it by little, testing the union costs fewer
+        // instructions than resolving 32 windows
+        const float dn = __ldg(wtab_row(A, rmax) + lane);
+        const float nb = (float)(sb[lane].end - sb[lane].start);
+        const float w_est = dn < 0.0f ? 0.0f : (dn >= 3.14159265f ? nb : dn * nb * 0.31830988f);
+        if (un <= kUnionSmall || (float)un <= w_est + (float)kShareSlack) cheap = 1;
       }
       cheap = __ballot_sync(FULL, cheap != 0);
     }
@@ -778,9 +800,11 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
         uint64_t kA0[kBandGroup], kA1[kBandGroup], kB0[kBandGroup];
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
-          kA0[u] = (w[u].sA < w[u].eA && w[u].tlA) ? __ldg(A.keys + w[u].sA) : 0;
-          kA1[u] = (w[u].sA < w[u].eA && w[u].thA <= kQMask) ? __ldg(A.keys + w[u].eA - 1) : 0;
-          kB0[u] = (w[u].sB < w[u].eB && w[u].tlB) ? __ldg(A.keys + w[u].sB) : 0;
+          if (kTrim) {
+            kA0[u] = (w[u].sA < w[u].eA && w[u].tlA) ? __ldg(A.keys + w[u].sA) : 0;
+            kA1[u] = (w[u].sA < w[u].eA && w[u].thA <= kQMask) ? __ldg(A.keys + w[u].eA - 1) : 0;
+            kB0[u] = (w[u].sB < w[u].eB && w[u].tlB) ? __ldg(A.keys + w[u].sB) : 0;
+          }
         }
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
@@ -790,7 +814,7 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
           if ((cheap >> j) & 1u) {
             r.sA = gA[u]; r.eA = gAe[u]; r.sB = gB[u]; r.eB = gBe[u];
           } else {
-            finish_trim(A.keys, r, kA0[u], kA1[u], kB0[u]);
+            if (kTrim) finish_trim(A.keys, r, kA0[u], kA1[u], kB0[u]);
             if (r.sB < r.eB && r.sB < r.eA) {  // window wraps onto itself: whole band
               r.sA = sb[j].start; r.eA = sb[j].end; r.sB = r.eB = 0;
             }
