@@ -1218,12 +1218,11 @@ constexpr int kCopyUnroll = 8;                  // loads in flight per lane
 // in k_light, whose hits k_light left back to back in the staging buffer,
 // row after row in candidate order.  With angular ids and no deferred query
 // in the tile the rows are also consecutive in the CSR: one straight copy.
-// Otherwise the warp copies the range into shared memory; with sample-order
-// ids each lane then sorts its row (<= kSmallSlots hits)
-// with a register network -- hrgen's Graph keeps rows sorted by id
+// Otherwise the warp stages groups of rows in shared memory; with
+// sample-order ids each lane then sorts its row (<= kSmallSlots hits) with a
+// register network -- hrgen's Graph keeps rows sorted by id
 // (graph.py:69-71); longer rows are queued for an in-place sort.  With
-// angular ids candidate order is id order and nothing is sorted.  Rows are
-// written out one at a time, 32 lanes wide.
+// angular ids candidate order is id order and nothing is sorted.
 template <bool kSampleIds>
 __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
@@ -1278,46 +1277,75 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
           if (i < T) idx[d0 + i] = x[u];
         }
       }
-    } else if (Htot <= kTileHits) {
-      // the tile's light rows are back to back in the staging buffer
-      // (k_light writes hits only): one coalesced copy into shared memory,
-      // row q at [hexcl_q, hexcl_q + len_q)
-      for (int32_t i0 = 0; i0 < T; i0 += 32 * kCopyUnroll) {
-        int32_t x[kCopyUnroll];
+    } else {
+      // Rows in groups of consecutive lanes whose hits fit in shared memory
+      // (one group for all but hub-heavy tiles): one coalesced copy of the
+      // group's staging range, row q at [hexcl_q - start, ...), the small
+      // rows sorted in registers (sample ids), rows written one at a time,
+      // 32 lanes wide.  A row above kTileHits alone is copied straight
+      // through.
+      __shared__ int64_t s_dst[kCompactThreads];
+      __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads];
+      const int wb = threadIdx.x - lane;
+      s_dst[threadIdx.x] = dst;
+      s_len[threadIdx.x] = len;
+      if (kSampleIds) push_job_warp(J, len > kSmallSlots, dst, len);
+      int l0 = 0;
+      while (l0 < 32) {
+        const int32_t start = __shfl_sync(FULL, hexcl, l0);
+        const unsigned fit = __ballot_sync(FULL, lane >= l0 && hi - start <= kTileHits);
+        if (!fit) {  // row l0 alone exceeds shared memory
+          const int64_t d = s_dst[wb + l0];
+          const int32_t n0 = s_len[wb + l0];
+          const int64_t s0 = base + start;
+          for (int32_t k0 = 0; k0 < n0; k0 += 32 * kCopyUnroll) {
+            int32_t x[kCopyUnroll];
 #pragma unroll
-        for (int u = 0; u < kCopyUnroll; ++u) {
-          const int32_t i = i0 + 32 * u + lane;
-          x[u] = i < T ? __ldg(A.stage + base + i) : 0;
-        }
+            for (int u = 0; u < kCopyUnroll; ++u) {
+              const int32_t k = k0 + 32 * u + lane;
+              x[u] = k < n0 ? __ldg(A.stage + s0 + k) : 0;
+            }
 #pragma unroll
-        for (int u = 0; u < kCopyUnroll; ++u) {
-          const int32_t i = i0 + 32 * u + lane;
-          if (i < T) sm[i] = x[u];
+            for (int u = 0; u < kCopyUnroll; ++u) {
+              const int32_t k = k0 + 32 * u + lane;
+              if (k < n0) idx[d + k] = x[u];
+            }
+          }
+          ++l0;
+          continue;
         }
-      }
-      __syncwarp();
-      if (kSampleIds) {
-        const bool small = len > 1 && len <= kSmallSlots;
-        push_job_warp(J, len > kSmallSlots, dst, len);
-        const int32_t mx = __reduce_max_sync(FULL, small ? len : 0);
-        if (mx <= 16) {
-          if (small) thread_sort_smem<16>(sm + hexcl, len, len);
-        } else if (mx <= 32) {
-          if (small) thread_sort_smem<32>(sm + hexcl, len, len);
-        } else if (kSmallSlots > 32) {
-          if (small) thread_sort_smem<kSmallSlots>(sm + hexcl, len, len);
+        const int l1 = 32 - __clz(fit);  // hits are non-decreasing: fit = lanes [l0, l1)
+        const int32_t G = __shfl_sync(FULL, hi, l1 - 1) - start;
+        const bool ing = lane >= l0 && lane < l1;
+        for (int32_t i0 = 0; i0 < G; i0 += 32 * kCopyUnroll) {
+          int32_t x[kCopyUnroll];
+#pragma unroll
+          for (int u = 0; u < kCopyUnroll; ++u) {
+            const int32_t i = i0 + 32 * u + lane;
+            x[u] = i < G ? __ldg(A.stage + base + start + i) : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kCopyUnroll; ++u) {
+            const int32_t i = i0 + 32 * u + lane;
+            if (i < G) sm[i] = x[u];
+          }
         }
+        s_off[threadIdx.x] = hexcl - start;
         __syncwarp();
-      }
-      {
-        __shared__ int64_t s_dst[kCompactThreads];
-        __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads];
-        const int wb = threadIdx.x - lane;
-        s_dst[threadIdx.x] = dst;
-        s_len[threadIdx.x] = len;
-        s_off[threadIdx.x] = hexcl;
-        __syncwarp();
-        unsigned todo = __ballot_sync(FULL, len > 0);
+        if (kSampleIds) {
+          const bool small = ing && len > 1 && len <= kSmallSlots;
+          const int32_t mx = __reduce_max_sync(FULL, small ? len : 0);
+          int32_t* row = sm + (hexcl - start);
+          if (mx <= 16) {
+            if (small) thread_sort_smem<16>(row, len, len);
+          } else if (mx <= 32) {
+            if (small) thread_sort_smem<32>(row, len, len);
+          } else if (kSmallSlots > 32) {
+            if (small) thread_sort_smem<kSmallSlots>(row, len, len);
+          }
+          __syncwarp();
+        }
+        unsigned todo = __ballot_sync(FULL, ing && len > 0);
         while (todo) {
           const int l = __ffs(todo) - 1;
           todo &= todo - 1;
@@ -1325,32 +1353,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
           const int32_t n0 = s_len[wb + l], e0 = s_off[wb + l];
           for (int32_t k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
         }
+        __syncwarp();
+        l0 = l1;
       }
-      __syncwarp();
-    } else {
-      // a hub-heavy tile: copy row by row straight into the CSR
-      unsigned todo = __ballot_sync(FULL, len > 0);
-      while (todo) {
-        const int l = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const int64_t d = __shfl_sync(FULL, dst, l);
-        const int32_t n0 = __shfl_sync(FULL, ns, l);
-        const int64_t s0 = __shfl_sync(FULL, src, l);
-        for (int32_t k0 = 0; k0 < n0; k0 += 32 * kCopyUnroll) {
-          int32_t x[kCopyUnroll];
-#pragma unroll
-          for (int u = 0; u < kCopyUnroll; ++u) {
-            const int32_t k = k0 + 32 * u + lane;
-            x[u] = k < n0 ? __ldg(A.stage + s0 + k) : 0;
-          }
-#pragma unroll
-          for (int u = 0; u < kCopyUnroll; ++u) {
-            const int32_t k = k0 + 32 * u + lane;
-            if (k < n0) idx[d + k] = x[u];
-          }
-        }
-      }
-      if (kSampleIds) push_job_warp(J, len > 1, dst, len);
     }
   }
 }
