@@ -294,9 +294,9 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSortWarpSmem));
-    CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<256, kBucketMax, 1>,
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<256, kBucketMax, kMidShift>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sort_rows_smem<kBucketMax, 1>()));
+                                  (int)sort_rows_smem<kBucketMax, kMidShift>()));
     CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<1024, kLargeMax, 2>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sort_rows_smem<kLargeMax, 2>()));
@@ -427,7 +427,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     const RowList none{nullptr, nullptr, nullptr};
     const unsigned sm = (unsigned)c->sm_count;
     k_sort_warp<<<8 * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
-    k_sort_rows<256, kBucketMax, 1><<<8 * sm, 256, sort_rows_smem<kBucketMax, 1>(), st>>>(
+    k_sort_rows<256, kBucketMax, kMidShift><<<8 * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(
         idx, idx, J.mid, J.large);
     k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
         idx, idx, J.large, G.rows);

@@ -53,6 +53,12 @@ namespace hrg {
 #ifndef HRG_UNION_SMALL
 #define HRG_UNION_SMALL 2
 #endif
+#ifndef HRG_WARP_SHIFT
+#define HRG_WARP_SHIFT 1
+#endif
+#ifndef HRG_MID_SHIFT
+#define HRG_MID_SHIFT 1
+#endif
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
 #endif
@@ -1471,8 +1477,9 @@ __device__ bool group_bucket_sort(const int32_t* in, int32_t* tmp, int32_t* cnt,
 
 constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
 constexpr int kSortWarpThreads = 256;
+constexpr int kWarpShift = HRG_WARP_SHIFT;  // warp bucket sort: len >> kWarpShift buckets
 struct SortWarpSmem {
-  int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[kWarpBucketMax / 2 + 1];
+  int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[(kWarpBucketMax >> kWarpShift) + 1];
   int flag;
 };
 constexpr size_t kSortWarpSmem = sizeof(SortWarpSmem) * (kSortWarpThreads / 32);
@@ -1511,7 +1518,7 @@ __global__ void __launch_bounds__(kSortWarpThreads) k_sort_warp(int32_t* __restr
     mn = __reduce_min_sync(FULL, mn);
     mx = __reduce_max_sync(FULL, mx);
     __syncwarp();
-    if (!group_bucket_sort<32, 1>(S.in, S.tmp, S.cnt, row, len, lane, mn, mx, &S.flag,
+    if (!group_bucket_sort<32, kWarpShift>(S.in, S.tmp, S.cnt, row, len, lane, mn, mx, &S.flag,
                                   nullptr)) {
       group_bitonic<32>(S.in, len, lane);
       for (int i = lane; i < len; i += 32) row[i] = S.in[i];
@@ -1521,6 +1528,7 @@ __global__ void __launch_bounds__(kSortWarpThreads) k_sort_warp(int32_t* __restr
 }
 
 constexpr int kBucketMax = 4096;   // rows a 256-thread block sorts
+constexpr int kMidShift = HRG_MID_SHIFT;
 constexpr int kLargeMax = 24576;   // rows a 1024-thread block sorts (in + out: 221 KB)
 template <int kCap, int kShift>
 constexpr size_t sort_rows_smem() { return sizeof(int32_t) * (2 * kCap + (kCap >> kShift) + 1); }
