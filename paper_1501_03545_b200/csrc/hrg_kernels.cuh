@@ -607,9 +607,10 @@ __device__ __forceinline__ Cand load_cand(const QueryArgs& A, const QFull& f, in
 // Edge {v, w} is decided by the circle of the smaller vertex id, exactly as
 // hrgen queries from v and keeps ids > v (generator.py:182-187).
 __device__ __forceinline__ bool pair_test(const QFull& f, const Cand& c, int32_t w) {
-  if (w == f.pos) return false;
-  if (c.lower) return ref_pred(f.px, f.py, c.d0, c.d1, c.d2);  // pred(w -> v)
-  return ref_pred(c.d0, c.d1, f.cx, f.cy, f.rsq);              // pred(v -> w)
+  const double x = c.lower ? f.px : c.d0, y = c.lower ? f.py : c.d1;  // pred(w -> v) :
+  const double cx = c.lower ? c.d0 : f.cx, cy = c.lower ? c.d1 : f.cy;  // pred(v -> w)
+  const double rs = c.lower ? c.d2 : f.rsq;
+  return ref_pred(x, y, cx, cy, rs) && w != f.pos;
 }
 
 __device__ __forceinline__ void load_bands(const QueryArgs& A, Band* sb) {
@@ -689,16 +690,22 @@ __device__ __forceinline__ LoadedCand load_walk_cand(const QueryArgs& A, int32_t
 template <bool kSampleIds>
 __device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, int32_t w,
                                           int32_t& id) {
+  // operands selected first, one predicate evaluation (no divergent branch):
+  // lower -> pred(w -> v) with w's circle, else pred(v -> w) with v's
   if (kSampleIds) {
     id = (int32_t)(__double_as_longlong(c.x.y) & 0xffffffffll);
-    if (id == f.idv) return false;
-    if (id < f.idv) return ref_pred(f.px, f.py, c.b.x, c.b.y, c.x.x);  // pred(w -> v)
-    return ref_pred(c.a.x, c.a.y, f.cx, f.cy, f.rsq);                   // pred(v -> w)
+    const bool lower = id < f.idv;
+    const double x = lower ? f.px : c.a.x, y = lower ? f.py : c.a.y;
+    const double cx = lower ? c.b.x : f.cx, cy = lower ? c.b.y : f.cy;
+    const double rs = lower ? c.x.x : f.rsq;
+    return ref_pred(x, y, cx, cy, rs) && id != f.idv;
   } else {
     id = w;
-    if (w == f.pos) return false;
-    if (w < f.pos) return ref_pred(f.px, f.py, c.a.x, c.a.y, c.b.x);
-    return ref_pred(c.a.x, c.a.y, f.cx, f.cy, f.rsq);
+    const bool lower = w < f.pos;
+    const double x = lower ? f.px : c.a.x, y = lower ? f.py : c.a.y;
+    const double cx = lower ? c.a.x : f.cx, cy = lower ? c.a.y : f.cy;
+    const double rs = lower ? c.b.x : f.rsq;
+    return ref_pred(x, y, cx, cy, rs) && w != f.pos;
   }
 }
 
