@@ -53,9 +53,6 @@ namespace hrg {
 #ifndef HRG_UNION_SMALL
 #define HRG_UNION_SMALL 2
 #endif
-#ifndef HRG_WARP_SHIFT
-#define HRG_WARP_SHIFT 1
-#endif
 #ifndef HRG_MID_SHIFT
 #define HRG_MID_SHIFT 1
 #endif
@@ -1484,17 +1481,28 @@ __device__ bool group_bucket_sort(const int32_t* in, int32_t* tmp, int32_t* cnt,
 
 constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
 constexpr int kSortWarpThreads = 256;
-constexpr int kWarpShift = HRG_WARP_SHIFT;  // warp bucket sort: len >> kWarpShift buckets
 struct SortWarpSmem {
-  int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[(kWarpBucketMax >> kWarpShift) + 1];
+  int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[32];
   int flag;
 };
 constexpr size_t kSortWarpSmem = sizeof(SortWarpSmem) * (kSortWarpThreads / 32);
 
+// One lane sorts its bucket b[0, c), c <= N, in registers (in place).
+template <int N>
+__device__ __forceinline__ void lane_sort_bucket(int32_t* b, int32_t c) {
+  int32_t x[N];
+#pragma unroll
+  for (int t = 0; t < N; ++t) x[t] = t < c ? b[t] : INT32_MAX;
+  reg_oddeven<N>(x);
+#pragma unroll
+  for (int t = 0; t < N; ++t)
+    if (t < c) b[t] = x[t];
+}
+
 // Queued rows (sample-order ids), one warp per row: up to 64 ids by a
 // register network, up to kWarpBucketMax by a bucket sort in shared memory;
 // longer rows go on to k_sort_rows.
-__global__ void __launch_bounds__(kSortWarpThreads) k_sort_warp(int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(kSortWarpThreads, 4) k_sort_warp(int32_t* __restrict__ idx,
                                                                 SortJobs J) {
   extern __shared__ __align__(16) unsigned char sort_smem[];
   SortWarpSmem& S = reinterpret_cast<SortWarpSmem*>(sort_smem)[threadIdx.x >> 5];
@@ -1524,12 +1532,43 @@ __global__ void __launch_bounds__(kSortWarpThreads) k_sort_warp(int32_t* __restr
     }
     mn = __reduce_min_sync(FULL, mn);
     mx = __reduce_max_sync(FULL, mx);
+    // 32 value buckets over [mn, mx], one per lane: count, scan, scatter into
+    // tmp, then each lane sorts its bucket (~len/32 ids) with a register
+    // network.  A bucket above 32 ids (far from uniform) -> bitonic fallback.
+    S.cnt[lane] = 0;
     __syncwarp();
-    if (!group_bucket_sort<32, kWarpShift>(S.in, S.tmp, S.cnt, row, len, lane, mn, mx, &S.flag,
-                                  nullptr)) {
+    const float scale = 32.0f / ((float)(mx - mn) + 1.0f);
+    for (int i = lane; i < len; i += 32)
+      atomicAdd(&S.cnt[min((int)((float)(S.in[i] - mn) * scale), 31)], 1);
+    __syncwarp();
+    const int32_t c = S.cnt[lane];
+    const int32_t cmax = __reduce_max_sync(FULL, c);
+    if (cmax > 32) {
       group_bitonic<32>(S.in, len, lane);
       for (int i = lane; i < len; i += 32) row[i] = S.in[i];
+      __syncwarp();
+      continue;
     }
+    int32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int32_t off = inc - c;
+    __syncwarp();
+    S.cnt[lane] = off;  // scatter cursors
+    __syncwarp();
+    for (int i = lane; i < len; i += 32) {
+      const int32_t x = S.in[i];
+      S.tmp[atomicAdd(&S.cnt[min((int)((float)(x - mn) * scale), 31)], 1)] = x;
+    }
+    __syncwarp();
+    if (cmax <= 8) lane_sort_bucket<8>(S.tmp + off, c);
+    else if (cmax <= 16) lane_sort_bucket<16>(S.tmp + off, c);
+    else lane_sort_bucket<32>(S.tmp + off, c);
+    __syncwarp();
+    for (int i = lane; i < len; i += 32) row[i] = S.tmp[i];
     __syncwarp();
   }
 }
