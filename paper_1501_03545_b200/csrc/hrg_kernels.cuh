@@ -54,7 +54,7 @@ namespace hrg {
 #define HRG_UNION_SMALL 2
 #endif
 #ifndef HRG_MID_SHIFT
-#define HRG_MID_SHIFT 1
+#define HRG_MID_SHIFT -1
 #endif
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
@@ -1574,10 +1574,12 @@ __global__ void __launch_bounds__(kSortWarpThreads, 4) k_sort_warp(int32_t* __re
 }
 
 constexpr int kBucketMax = 4096;   // rows a 256-thread block sorts
-constexpr int kMidShift = HRG_MID_SHIFT;
+constexpr int kMidShift = HRG_MID_SHIFT;  // < 0: one bucket per thread, register networks
 constexpr int kLargeMax = 24576;   // rows a 1024-thread block sorts (in + out: 221 KB)
 template <int kCap, int kShift>
-constexpr size_t sort_rows_smem() { return sizeof(int32_t) * (2 * kCap + (kCap >> kShift) + 1); }
+constexpr size_t sort_rows_smem() {
+  return sizeof(int32_t) * (2 * kCap + (kShift < 0 ? 1024 : (kCap >> kShift) + 1));
+}
 
 // Rows of up to kCap ids, one block of kThreads per row, in shared memory
 // (bucket sort, bitonic fallback).  Rows above kCap are pushed to `over`
@@ -1629,8 +1631,60 @@ __global__ void __launch_bounds__(kThreads) k_sort_rows(const int32_t* src_base,
     mx = __reduce_max_sync(0xffffffffu, mx);
     if (lane == 0) { atomicMin(&s_min, mn); atomicMax(&s_max, mx); }
     __syncthreads();
-    if (!group_bucket_sort<kThreads, kShift>(in, out, cnt, dst, len, tid, s_min, s_max, &s_flag,
-                                              s_wsum)) {
+    if (kShift < 0) {
+      // one value bucket per thread (~len / kThreads ids), sorted by that
+      // thread with a register network
+      mn = s_min;
+      const float scale = (float)kThreads / ((float)(s_max - mn) + 1.0f);
+      cnt[tid] = 0;
+      if (tid == 0) s_flag = 0;
+      __syncthreads();
+      for (int i = tid; i < len; i += kThreads)
+        atomicAdd(&cnt[min((int)((float)(in[i] - mn) * scale), kThreads - 1)], 1);
+      __syncthreads();
+      const int32_t c = cnt[tid];
+      const int32_t cm = __reduce_max_sync(0xffffffffu, c);
+      if (lane == 0) atomicMax(&s_flag, cm);
+      int32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) s_wsum[tid >> 5] = inc;
+      __syncthreads();
+      if (tid < 32) {
+        const int32_t w = tid < kThreads / 32 ? s_wsum[tid] : 0;
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (tid >= o) wi += y;
+        }
+        if (tid < kThreads / 32) s_wsum[tid] = wi - w;
+      }
+      __syncthreads();
+      const int32_t cmax = s_flag;
+      const int32_t boff = s_wsum[tid >> 5] + inc - c;
+      if (cmax <= 32) {
+        cnt[tid] = boff;
+        __syncthreads();
+        for (int i = tid; i < len; i += kThreads) {
+          const int32_t x = in[i];
+          out[atomicAdd(&cnt[min((int)((float)(x - mn) * scale), kThreads - 1)], 1)] = x;
+        }
+        __syncthreads();
+        if (cmax <= 8) lane_sort_bucket<8>(out + boff, c);
+        else if (cmax <= 16) lane_sort_bucket<16>(out + boff, c);
+        else lane_sort_bucket<32>(out + boff, c);
+        __syncthreads();
+        for (int i = tid; i < len; i += kThreads) dst[i] = out[i];
+      } else {
+        group_bitonic<kThreads>(in, len, tid);
+        for (int i = tid; i < len; i += kThreads) dst[i] = in[i];
+      }
+    } else if (!group_bucket_sort<kThreads, kShift < 0 ? 0 : kShift>(
+                   in, out, cnt, dst, len, tid, s_min, s_max, &s_flag, s_wsum)) {
       group_bitonic<kThreads>(in, len, tid);
       for (int i = tid; i < len; i += kThreads) dst[i] = in[i];
     }
