@@ -1224,6 +1224,16 @@ constexpr int kSmallSlots = HRG_SMALL_SLOTS;    // rows sorted by one thread (32
 constexpr int kTileHits = 2048;                 // smem hits per warp
 constexpr int kCopyUnroll = 8;                  // loads in flight per lane
 
+// 4-byte global -> shared copy that bypasses registers (LDGSTS).
+__device__ __forceinline__ void cp_async4(int32_t* smem, const int32_t* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // Compaction of light rows.  A warp owns the same 32 consecutive queries as
 // in k_light, whose hits k_light left back to back in the staging buffer,
 // row after row in candidate order.  With angular ids and no deferred query
@@ -1327,19 +1337,10 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
         const int l1 = 32 - __clz(fit);  // hits are non-decreasing: fit = lanes [l0, l1)
         const int32_t G = __shfl_sync(FULL, hi, l1 - 1) - start;
         const bool ing = lane >= l0 && lane < l1;
-        for (int32_t i0 = 0; i0 < G; i0 += 32 * kCopyUnroll) {
-          int32_t x[kCopyUnroll];
-#pragma unroll
-          for (int u = 0; u < kCopyUnroll; ++u) {
-            const int32_t i = i0 + 32 * u + lane;
-            x[u] = i < G ? __ldg(A.stage + base + start + i) : 0;
-          }
-#pragma unroll
-          for (int u = 0; u < kCopyUnroll; ++u) {
-            const int32_t i = i0 + 32 * u + lane;
-            if (i < G) sm[i] = x[u];
-          }
-        }
+        // asynchronous copies (no registers held): the whole group in flight
+        const int32_t* gsrc = A.stage + base + start;
+        for (int32_t i = lane; i < G; i += 32) cp_async4(sm + i, gsrc + i);
+        cp_async_wait_all();
         s_off[threadIdx.x] = hexcl - start;
         __syncwarp();
         if (kSampleIds) {
