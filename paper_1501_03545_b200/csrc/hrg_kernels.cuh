@@ -1284,15 +1284,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
     if (!kSampleIds && __all_sync(FULL, !active || light)) {
       // angular ids, every query light: staging range == CSR range
       const int64_t d0 = __shfl_sync(FULL, dst, 0);
-      for (int32_t i0 = 0; i0 < T; i0 += 32 * kCopyUnroll) {
-        int32_t x[kCopyUnroll];
+      constexpr int U = 2 * kCopyUnroll;
+      for (int32_t i0 = 0; i0 < T; i0 += 32 * U) {
+        int32_t x[U];
 #pragma unroll
-        for (int u = 0; u < kCopyUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int32_t i = i0 + 32 * u + lane;
           x[u] = i < T ? __ldg(A.stage + base + i) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < kCopyUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int32_t i = i0 + 32 * u + lane;
           if (i < T) idx[d0 + i] = x[u];
         }
