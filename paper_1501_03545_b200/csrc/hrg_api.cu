@@ -71,9 +71,9 @@ struct hrg_context {
   // coordinates in vertex-id order
   Buf phi, rn, rp;
   // sort
-  Buf keys_in, keys_out, vals_in, vals_out;
+  Buf keys_out, vals_in, vals_out;
   // sorted records
-  Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn;
+  Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn, pr;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
@@ -125,9 +125,11 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   size_t d = sizeof(double) * (size_t)n, f = sizeof(float) * (size_t)n, i32 = 4 * (size_t)n;
   size_t u64 = 8 * (size_t)n;
   CUDA_TRY(c->phi.ensure(d)); CUDA_TRY(c->rn.ensure(d)); CUDA_TRY(c->rp.ensure(d));
-  CUDA_TRY(c->keys_in.ensure(u64)); CUDA_TRY(c->keys_out.ensure(u64));
+  CUDA_TRY(c->keys_out.ensure(u64));
+  CUDA_TRY(c->k32_in.ensure(i32)); CUDA_TRY(c->k32_out.ensure(i32));
   CUDA_TRY(c->vals_in.ensure(i32)); CUDA_TRY(c->vals_out.ensure(i32));
   for (Buf* b : {&c->s_phi, &c->s_rp, &c->s_rn}) CUDA_TRY(b->ensure(d));
+  CUDA_TRY(c->pr.ensure(2 * d));
   CUDA_TRY(c->pt.ensure(16 * (size_t)n));
   CUDA_TRY(c->circ.ensure(sizeof(Circ) * (size_t)n));
   CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
@@ -155,10 +157,6 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                        const hrg_shard* shard, double C, bool sample_ids) {
   int64_t n = M->n;
   cudaStream_t st = c->stream;
-  CUDA_TRY(c->k32_in.ensure(4 * (size_t)n));
-  CUDA_TRY(c->k32_out.ensure(4 * (size_t)n));
-  k_sort_keys32<<<blocks_for(n), 256, 0, st>>>(n, c->keys_in.as<uint64_t>(),
-                                               c->k32_in.as<uint32_t>());
   size_t tb = 0;
   CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->k32_in.as<uint32_t>(),
                                            c->k32_out.as<uint32_t>(), c->vals_in.as<int32_t>(),
@@ -173,19 +171,15 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
                   c->vals_out.as<int32_t>()};
   if (sample_ids)
-    k_gather<true><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(),
-                                                  c->keys_in.as<uint64_t>(),
-                                                  c->keys_out.as<uint64_t>(), c->phi.as<double>(),
-                                                  c->rp.as<double>(), c->rn.as<double>(),
-                                                  M->cosh_r_minus_1, recs, q,
-                                                  c->s_rp.as<double>(), c->s_rn.as<double>());
+    k_gather<true><<<blocks_for(n), 256, 0, st>>>(
+        n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
+        c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
+        nullptr);
   else
-    k_gather<false><<<blocks_for(n), 256, 0, st>>>(n, c->vals_out.as<int32_t>(),
-                                                   c->keys_in.as<uint64_t>(),
-                                                   c->keys_out.as<uint64_t>(), c->phi.as<double>(),
-                                                   c->rp.as<double>(), c->rn.as<double>(),
-                                                   M->cosh_r_minus_1, recs, q,
-                                                   c->s_rp.as<double>(), c->s_rn.as<double>());
+    k_gather<false><<<blocks_for(n), 256, 0, st>>>(
+        n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
+        c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
+        c->s_rn.as<double>());
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     // sector bounds on the sort granularity (multiples of 2^kSortShift)
@@ -471,13 +465,14 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   if (!from_coords) {
     SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
     k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
-                                            c->rp.as<double>(), c->keys_in.as<uint64_t>(),
-                                            c->vals_in.as<int32_t>());
+                                            c->rp.as<double>(), c->k32_in.as<uint32_t>(),
+                                            c->vals_in.as<int32_t>(), c->pr.as<double2>());
   } else {
     CUDA_TRY(cudaMemsetAsync(c->bad.p, 0, 4, st));
     k_keys_from_coords<<<blocks_for(n), 256, 0, st>>>(
         n, c->phi.as<double>(), c->rp.as<double>(), M->max_r, C, S, c->rn.as<double>(),
-        c->keys_in.as<uint64_t>(), c->vals_in.as<int32_t>(), c->bad.as<int>());
+        c->k32_in.as<uint32_t>(), c->vals_in.as<int32_t>(), c->bad.as<int>(),
+        c->pr.as<double2>());
     int bad = 0;
     CUDA_TRY(cudaMemcpyAsync(&bad, c->bad.p, 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -533,8 +528,8 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   if (!c) return HRG_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_in, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->stage,
+  for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_out, &c->vals_in, &c->vals_out,
+                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
@@ -643,8 +638,8 @@ hrg_status hrg_sample_points(hrg_context* c, const hrg_model* M, uint64_t seed, 
   double C = std::ldexp(1.0, kQBits) / kTwoPi;
   SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
   k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
-                                          c->rp.as<double>(), c->keys_in.as<uint64_t>(),
-                                          c->vals_in.as<int32_t>());
+                                          c->rp.as<double>(), c->k32_in.as<uint32_t>(),
+                                          c->vals_in.as<int32_t>(), c->pr.as<double2>());
   CUDA_TRY(cudaGetLastError());
   const double *sp = c->phi.as<double>(), *sn = c->rn.as<double>(), *sr = c->rp.as<double>();
   if (order == HRG_ORDER_ANGULAR) {

@@ -107,14 +107,27 @@ struct SampleParams {
   double C;  // 2^53 / (2 pi)
 };
 
+// Sort key: band << 27 | top 27 bits of the angular key.  Points are ordered
+// by (band, angle) to 2^-27 of a turn; ties keep draw order (stable sort).
+// Everything that relies on the order works at that granularity or coarser:
+// directory buckets (shift >= kSortShift), shard sector bounds (multiples of
+// 2^kSortShift) and the exact key trims, which drop a point only on its own
+// full key and so stay correct on any order.
+constexpr int kSortShift = kQBits - 27;
+constexpr int kDirExtra = HRG_DIR_EXTRA;  // directory buckets per point: 1-2 x 2^kDirExtra
+__device__ __forceinline__ uint32_t sort_key32(int band, uint64_t q) {
+  return ((uint32_t)band << 27) | (uint32_t)(q >> kSortShift);
+}
+
 // hrgen generator.py:160-179 with a counter-based stream: vertex i draws its
 // angle from the first and its radius from the second 53-bit uniform of
 // Philox4x32-10(counter = i, key = seed).
 __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandSpec S,
                                                 double* __restrict__ phi, double* __restrict__ rn,
                                                 double* __restrict__ rp,
-                                                uint64_t* __restrict__ keys,
-                                                int32_t* __restrict__ vals) {
+                                                uint32_t* __restrict__ keys,
+                                                int32_t* __restrict__ vals,
+                                                double2* __restrict__ pr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t c[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 0u, 0u};
@@ -127,7 +140,8 @@ __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandS
   r = fmin(r, P.r_cap);                                                // :174
   double p = fmin(tanh(__dmul_rn(r, 0.5)), P.rp_cap);                 // :175-178
   phi[i] = ph; rn[i] = r; rp[i] = p;
-  keys[i] = ((uint64_t)band_of(S, p) << kQBits) | qkey(ph, P.C);
+  pr[i] = make_double2(ph, p);
+  keys[i] = sort_key32(band_of(S, p), qkey(ph, P.C));
   vals[i] = (int32_t)i;
 }
 
@@ -137,15 +151,17 @@ __global__ void __launch_bounds__(256) k_keys_from_coords(int64_t n, const doubl
                                                           const double* __restrict__ rp,
                                                           double max_r, double C, BandSpec S,
                                                           double* __restrict__ rn,
-                                                          uint64_t* __restrict__ keys,
+                                                          uint32_t* __restrict__ keys,
                                                           int32_t* __restrict__ vals,
-                                                          int* __restrict__ bad) {
+                                                          int* __restrict__ bad,
+                                                          double2* __restrict__ pr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ph = phi[i], p = rp[i];
   if (!(ph >= 0.0 && ph < kTwoPi && p >= 0.0 && p < max_r)) { atomicOr(bad, 1); p = 0.0; ph = 0.0; }
   rn[i] = 2.0 * atanh(p);  // geometry.py:121 to_native_radius
-  keys[i] = ((uint64_t)band_of(S, p) << kQBits) | qkey(ph, C);
+  pr[i] = make_double2(ph, p);
+  keys[i] = sort_key32(band_of(S, p), qkey(ph, C));
   vals[i] = (int32_t)i;
 }
 
@@ -181,29 +197,14 @@ struct QRec {          // query-side extras, per sorted position
 // Gather into (band, angle) order and precompute every per-point quantity the
 // query needs.  p_x/p_y: quadtree.py:474-475; c_x/c_y/rad^2: quadtree.py:516-518
 // with center_r/rad from geometry.py:141-157.
-// Sort key: band << 27 | top 27 bits of the angular key.  Points are ordered
-// by (band, angle) to 2^-27 of a turn; ties keep draw order (stable sort).
-// Everything that relies on the order works at that granularity or coarser:
-// directory buckets (shift >= kSortShift), shard sector bounds (multiples of
-// 2^kSortShift) and the exact key trims, which drop a point only on its own
-// full key and so stay correct on any order.
-constexpr int kSortShift = kQBits - 27;
-constexpr int kDirExtra = HRG_DIR_EXTRA;  // directory buckets per point: 1-2 x 2^kDirExtra
-__global__ void __launch_bounds__(256) k_sort_keys32(int64_t n, const uint64_t* __restrict__ keys,
-                                                     uint32_t* __restrict__ k32) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) {
-    const uint64_t k = keys[i];
-    k32[i] = (uint32_t)((k >> kQBits) << 27) | (uint32_t)((k & kQMask) >> kSortShift);
-  }
-}
-
+// (phi, r_p) arrive packed (one 16 B random read per point, the DRAM burst
+// granularity, instead of one per array); the full key is rebuilt from the
+// band bits of the sort key and qkey(phi), the same function k_sample used.
 template <bool kSampleIds>
 __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __restrict__ perm,
-                                                const uint64_t* __restrict__ keys_in,
-                                                uint64_t* __restrict__ keys_out,
-                                                const double* __restrict__ phi,
-                                                const double* __restrict__ rp,
+                                                const uint32_t* __restrict__ k32,
+                                                uint64_t* __restrict__ keys_out, double C,
+                                                const double2* __restrict__ pr,
                                                 const double* __restrict__ rn, double a,
                                                 Recs rec, QRec q,
                                                 double* __restrict__ s_rp,
@@ -211,8 +212,9 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __rest
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   int32_t i = perm[p];
-  keys_out[p] = keys_in[i];
-  double ph = phi[i], r = rp[i];
+  const double2 q2 = pr[i];
+  const double ph = q2.x, r = q2.y;
+  keys_out[p] = ((uint64_t)(k32[p] >> 27) << kQBits) | qkey(ph, C);
   double sn, cs;
   sincos_cr(ph, &sn, &cs);
   double cr, rad;
