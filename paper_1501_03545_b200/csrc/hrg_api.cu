@@ -75,7 +75,7 @@ struct hrg_context {
   // sorted records
   Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn, pr;
   // staging + heavy queries
-  Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits,
+  Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits, chunk_entry,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
       sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_dst, job_len, mid_off, mid_len;
   int64_t stage_cap = 0;
@@ -330,6 +330,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       CUDA_TRY(c->chunk_hits.ensure(4 * (size_t)total_chunks));
+      CUDA_TRY(c->chunk_entry.ensure(4 * (size_t)total_chunks));
+      k_chunk_owner<<<blocks_for(H), 256, 0, st>>>(c->chunk_start.as<int64_t>(), H,
+                                                   c->chunk_entry.as<int32_t>());
+      A.chunk_entry = c->chunk_entry.as<int32_t>();
       A.chunk_start = c->chunk_start.as<int64_t>();
       A.chunk_hits = c->chunk_hits.as<int32_t>();
       A.total_chunks = total_chunks;
@@ -337,7 +341,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
           1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
       if (sample_ids) k_heavy<true><<<gh, 256, 0, st>>>(A, H);
       else k_heavy<false><<<gh, 256, 0, st>>>(A, H);
-      launches += 2;
+      launches += 3;
     }
     CUDA_TRY(cudaEventRecord(c->ev[E_COUNTED], st));
     CUDA_TRY(cudaGetLastError());
@@ -531,7 +535,8 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_out, &c->vals_in, &c->vals_out,
                  &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
-                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_off, &c->slots,
+                 &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_entry, &c->chunk_off,
+                 &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad,

@@ -384,6 +384,7 @@ struct QueryArgs {
   unsigned* heavy_n;
   int32_t* heavy_of;         // sorted position -> entry, or -1
   const int64_t* chunk_start;// entry -> first chunk (exclusive scan, H + 1)
+  const int32_t* chunk_entry;// chunk -> entry
   int64_t total_chunks;
   int32_t* chunk_hits;
   int32_t* deg;              // row length per vertex id
@@ -965,6 +966,14 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
   if (lane == 0 && cand_local) atomicAdd(A.cand_total, cand_local);
 }
 
+// chunk -> heavy entry (the inverse of chunk_start)
+__global__ void k_chunk_owner(const int64_t* __restrict__ chunk_start, int64_t H,
+                              int32_t* __restrict__ chunk_entry) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= H) return;
+  for (int64_t c = chunk_start[e]; c < chunk_start[e + 1]; ++c) chunk_entry[c] = (int32_t)e;
+}
+
 __global__ void k_heavy_chunks(const int32_t* __restrict__ heavy_c, int64_t H,
                                int32_t* __restrict__ nchunks) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -985,12 +994,7 @@ __global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
-    int64_t lo = 0, hi = H;  // entry: largest e with chunk_start[e] <= c
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) >> 1;
-      if (A.chunk_start[mid] <= c) lo = mid; else hi = mid;
-    }
-    const int64_t e = lo;
+    const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
     const int64_t local = c - A.chunk_start[e];
     QFull f = load_query<kSampleIds>(A, v);
@@ -1877,12 +1881,7 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
-    int64_t lo = 0, hi = H;
-    while (hi - lo > 1) {
-      int64_t mid = (lo + hi) >> 1;
-      if (A.chunk_start[mid] <= c) lo = mid; else hi = mid;
-    }
-    const int64_t e = lo;
+    const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
     const int32_t idv = sample_ids ? __ldg(A.rec.ids + v) : v;
     const int64_t c0 = A.chunk_start[e];
