@@ -985,7 +985,7 @@ __global__ void k_heavy_chunks(const int32_t* __restrict__ heavy_c, int64_t H,
 // at a time (4 batches in flight) with ballot-ordered writes into the
 // chunk's slot of the query's staging slice.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(256) k_heavy(QueryArgs A, int64_t H) {
+__global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
   __shared__ Band sb[kMaxBands];
   if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
   __syncthreads();
