@@ -279,11 +279,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   }
 
   if (c->grid_light == 0) {
-    CUDA_TRY(cudaFuncSetAttribute(k_light<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(LightSmem)));
-    CUDA_TRY(cudaFuncSetAttribute(k_light<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(LightSmem)));
-    c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads, sizeof(LightSmem));
+    c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -311,8 +307,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
-    if (sample_ids) k_light<true><<<gq, kLightThreads, sizeof(LightSmem), st>>>(A);
-    else k_light<false><<<gq, kLightThreads, sizeof(LightSmem), st>>>(A);
+    if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
+    else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
     launches++;
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
     CUDA_TRY(cudaGetLastError());

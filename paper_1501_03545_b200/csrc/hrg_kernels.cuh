@@ -727,8 +727,7 @@ __device__ __forceinline__ const QFull& f_of(const LightSmem& sm, int q) { retur
 template <bool kSampleIds>
 __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(QueryArgs A) {
   __shared__ Band sb[kMaxBands];
-  extern __shared__ __align__(16) unsigned char light_smem[];
-  LightSmem& sm = *reinterpret_cast<LightSmem*>(light_smem);
+  __shared__ LightSmem sm;
   load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
