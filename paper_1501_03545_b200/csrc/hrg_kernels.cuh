@@ -56,6 +56,12 @@ namespace hrg {
 #ifndef HRG_MID_SHIFT
 #define HRG_MID_SHIFT -1
 #endif
+#ifndef HRG_ELEM_WRITE
+#define HRG_ELEM_WRITE 1
+#endif
+#ifndef HRG_COMPACT_MINB
+#define HRG_COMPACT_MINB 5
+#endif
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
 #endif
@@ -1225,6 +1231,7 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
 }
 
 constexpr int kCompactThreads = 128;
+constexpr bool kElemWrite = HRG_ELEM_WRITE;  // compaction writes rows element-parallel
 constexpr int kSmallSlots = HRG_SMALL_SLOTS;    // rows sorted by one thread (32 or 64)
 constexpr int kTileHits = 2048;                 // smem hits per warp
 constexpr int kCopyUnroll = 8;                  // loads in flight per lane
@@ -1249,7 +1256,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // (graph.py:69-71); longer rows are queued for an in-place sort.  With
 // angular ids candidate order is id order and nothing is sorted.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(kCompactThreads) k_compact_light(
+__global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_light(
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
   __shared__ Band sb[kMaxBands];
   __shared__ int32_t buf[kCompactThreads / 32][kTileHits];
@@ -1310,8 +1317,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
       // rows sorted in registers (sample ids), rows written one at a time,
       // 32 lanes wide.  A row above kTileHits alone is copied straight
       // through.
-      __shared__ int64_t s_dst[kCompactThreads];
-      __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads];
+      __shared__ int64_t s_dst[kCompactThreads], r_dst[kCompactThreads];
+      __shared__ int32_t s_len[kCompactThreads], s_off[kCompactThreads], r_off[kCompactThreads];
       const int wb = threadIdx.x - lane;
       s_dst[threadIdx.x] = dst;
       s_len[threadIdx.x] = len;
@@ -1362,13 +1369,39 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact_light(
           }
           __syncwarp();
         }
-        unsigned todo = __ballot_sync(FULL, ing && len > 0);
-        while (todo) {
-          const int l = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int64_t d = s_dst[wb + l];
-          const int32_t n0 = s_len[wb + l], e0 = s_off[wb + l];
-          for (int32_t k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
+        if (kElemWrite) {
+          // write out element-parallel: lane l takes element i0 + l; its row
+          // (by rank among the group's non-empty rows) from a bit mask of the
+          // row starts inside the step
+          const bool nz = ing && len > 0;
+          const unsigned nzm = __ballot_sync(FULL, nz);
+          const int nr = __popc(nzm);
+          if (nz) {
+            const int rk = __popc(nzm & ((1u << lane) - 1u));
+            r_dst[wb + rk] = dst;
+            r_off[wb + rk] = hexcl - start;
+          }
+          __syncwarp();
+          int k0 = 0;  // rank of the row holding element i0
+          for (int32_t i0 = 0; i0 < G; i0 += 32) {
+            const int sl = k0 + 1 + lane;
+            const int32_t st = sl < nr ? r_off[wb + sl] : INT32_MAX;
+            const unsigned rel = (unsigned)(st - i0);
+            const unsigned mask = __reduce_or_sync(FULL, rel < 32u ? 1u << rel : 0u);
+            const int my = k0 + __popc(mask & ((2u << lane) - 1u));
+            k0 += __popc(mask);
+            const int32_t i = i0 + lane;
+            if (i < G) idx[r_dst[wb + my] + (i - r_off[wb + my])] = sm[i];
+          }
+        } else {
+          unsigned todo = __ballot_sync(FULL, ing && len > 0);
+          while (todo) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t d = s_dst[wb + l];
+            const int32_t n0 = s_len[wb + l], e0 = s_off[wb + l];
+            for (int32_t k = lane; k < n0; k += 32) idx[d + k] = sm[e0 + k];
+          }
         }
         __syncwarp();
         l0 = l1;
