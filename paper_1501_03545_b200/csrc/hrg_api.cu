@@ -6,7 +6,8 @@
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_select.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
@@ -14,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 #include <vector>
 
 #include "../../include/hrgen_b200.h"
@@ -80,12 +82,16 @@ struct hrg_context {
       sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_dst, job_len, mid_off, mid_len;
   int64_t stage_cap = 0;
   // index
-  Buf bands, dir, dir_total, bad;
+  Buf bands, dir, dir_total, bad, dir_gaps;
   // CSR
   Buf deg, rowptr, idx, idx2, cand;
-  Buf temp, k32_in, k32_out;
+  Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep;
   Buf widen;
-  int64_t n = 0, nnz = 0;
+  int64_t n = 0, np = 0, nnz = 0;
+  const float* sh_cover = nullptr;  // sharded subset: per-band circle coverage,
+  const int64_t* sh_lo = nullptr;   //   needed key ranges (k_shard_ranges)
+  const int64_t* sh_hi = nullptr;
+  const int* sh_mode = nullptr;
   bool have_result = false;
   bool coords_sorted = false;  // angular order: coordinates live in s_phi/s_rn/s_rp
   int32_t* idx_final = nullptr;
@@ -139,7 +145,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
   CUDA_TRY(c->dir.ensure(4 * (size_t)((2 * n << kDirExtra) + 2 * kMaxBands + 64)));
-  CUDA_TRY(c->dir_total.ensure(8)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
+  CUDA_TRY(c->dir_total.ensure(16)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
   CUDA_TRY(c->deg.ensure(i32)); CUDA_TRY(c->rowptr.ensure(8 * (size_t)(n + 1)));
   return HRG_OK;
 }
@@ -155,7 +161,7 @@ double ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // Sort keys -> permutation; build the sorted SoA, band table and directory.
 hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, int L,
                        const hrg_shard* shard, double C, bool sample_ids) {
-  int64_t n = M->n;
+  const int64_t n = c->np;  // indexed points (all, or a sharded run's subset)
   cudaStream_t st = c->stream;
   size_t tb = 0;
   CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, c->k32_in.as<uint32_t>(),
@@ -192,15 +198,23 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
     qhi <<= kSortShift;
   }
   k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
-                                 c->dir_total.as<int64_t>());
+                                 c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr);
   k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(
       n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(), c->s_bf.as<float>(),
       c->s_rp.as<double>(), c->bands.as<Band>());
   k_band_finish<<<1, 64, 0, st>>>(c->bands.as<Band>(), L);
+  CUDA_TRY(c->dir_gaps.ensure(sizeof(DirGap) * (size_t)(n / 16 + 2 * kMaxBands + 8)));
+  unsigned* ngaps = reinterpret_cast<unsigned*>(c->dir_total.as<char>() + 8);
+  CUDA_TRY(cudaMemsetAsync(ngaps, 0, 4, st));
   k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
-                                            c->dir.as<int32_t>());
+                                            c->dir.as<int32_t>(), c->dir_gaps.as<DirGap>(), ngaps);
+  const bool sharded = c->np < M->n;
+  const ShardRanges R{c->sh_lo, c->sh_hi, c->sh_mode};
+  k_dir_gaps<<<4 * c->sm_count, 256, 0, st>>>(c->dir_gaps.as<DirGap>(), ngaps,
+                                              c->bands.as<Band>(), c->dir.as<int32_t>(), R,
+                                              sharded);
   k_dir_tail<<<L, 256, 0, st>>>(c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
-                                c->dir.as<int32_t>());
+                                c->dir.as<int32_t>(), R, sharded);
   CUDA_TRY(cudaGetLastError());
   return HRG_OK;
 }
@@ -230,7 +244,8 @@ hrg_status scan_i32_to_i64(hrg_context* c, const int32_t* in, int64_t* out, int6
 // are not positions).
 hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool sample_ids,
                       hrg_stats* stats) {
-  int64_t n = M->n;
+  const int64_t n = M->n;   // vertex ids (rows)
+  const int64_t np = c->np; // indexed positions
   cudaStream_t st = c->stream;
   QueryArgs A;
   memset(&A, 0, sizeof(A));
@@ -268,7 +283,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   // (interleaving the bands' tiles by angle cuts DRAM reads by 40% but
   // measured slower: the tiles in flight then mix wide and narrow windows)
   {
-    const int64_t ntmax = n / 32 + L + 1;
+    const int64_t ntmax = np / 32 + L + 1;
     CUDA_TRY(c->tk0.ensure(8 * (size_t)ntmax));
     CUDA_TRY(c->tv0.ensure(8 * (size_t)ntmax));
     k_tile_keys<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
@@ -292,12 +307,12 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                   (int)sort_rows_smem<kLargeMax, 2>()));
   }
   unsigned gq = (unsigned)std::max<int64_t>(
-      1, std::min<int64_t>(blocks_for(n, kLightThreads), c->grid_light));
+      1, std::min<int64_t>(blocks_for(np, kLightThreads), c->grid_light));
   unsigned gc = (unsigned)std::max<int64_t>(
-      1, std::min<int64_t>(blocks_for(n, kCompactThreads), c->grid_compact));
+      1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
   // generous estimate; an overflow is detected and the pass re-run
-  if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * n, 1 << 20);
+  if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * np, 1 << 20);
   int64_t H = 0, total_chunks = 0, nnz = 0;
   unsigned long long ctr[8];
   for (int attempt = 0; attempt < 3; ++attempt) {
@@ -358,7 +373,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   int32_t* idx = c->idx.as<int32_t>();
   const int64_t* rp = c->rowptr.as<int64_t>();
   // sort jobs (sample order): light rows above kSmallSlots ids, heavy rows
-  const int64_t jcap = n + H + 1;
+  const int64_t jcap = np + H + 1;
   const int64_t mcap = nnz / (kWarpBucketMax + 1) + 1;
   const int64_t lcap = nnz / (kBucketMax + 1) + 1;
   CUDA_TRY(c->job_dst.ensure(8 * (size_t)jcap));
@@ -447,6 +462,91 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   return HRG_OK;
 }
 
+// Sharded runs (sample ids): index only the points some query of this
+// rank's sector can reach -- per band, the sector widened by the widest
+// window of any query radius present.  Keys and ids
+// of the kept points are compacted in draw order, so the sort and everything
+// after it see a smaller, identically ordered point set; ids stay global.
+hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, int L,
+                        const hrg_shard* shard) {
+  const int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  // smallest Poincare radius present (the widest windows)
+  CUDA_TRY(c->sh_buf.ensure(1024));
+  double* d_min = reinterpret_cast<double*>(c->sh_buf.p);
+  size_t tb = 0;
+  CUDA_TRY(cub::DeviceReduce::Min(nullptr, tb, c->rp.as<double>(), d_min, (int)n, st));
+  CUDA_TRY(c->temp.ensure(tb));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceReduce::Min(c->temp.p, tb, c->rp.as<double>(), d_min, (int)n, st));
+  double pmin = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&pmin, d_min, 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const double rmin = std::max(0.0, 2.0 * std::atanh(pmin) * (1.0 - 1e-12) - 1e-9);
+  // window table on bands whose innermost radius is their threshold
+  std::vector<Band> tbands(L);
+  for (int j = 0; j < L; ++j) {
+    memset(&tbands[j], 0, sizeof(Band));
+    tbands[j].start = 0;
+    tbands[j].end = 1;
+    tbands[j].pmin = j == 0 ? 0.0 : S.thr[j];
+  }
+  const int rows = (int)std::ceil(M->R / (double)kRowStep) + 2;
+  CUDA_TRY(c->sh_bands.ensure(sizeof(Band) * L));
+  CUDA_TRY(c->sh_wtab.ensure(sizeof(float) * (size_t)rows * L));
+  CUDA_TRY(cudaMemcpyAsync(c->sh_bands.p, tbands.data(), sizeof(Band) * L,
+                           cudaMemcpyHostToDevice, st));
+  k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
+                                      std::ldexp(1.0, -45), c->sh_wtab.as<float>());
+  const int64_t span = (int64_t)1 << 27;
+  const int64_t sec_lo = ((int64_t)shard->index * span + shard->count - 1) / shard->count;
+  const int64_t sec_hi = shard->index + 1 == shard->count
+                             ? span
+                             : ((int64_t)(shard->index + 1) * span + shard->count - 1) /
+                                   shard->count;
+  int64_t* lo = reinterpret_cast<int64_t*>(c->sh_buf.as<char>() + 64);
+  int64_t* hi = lo + kMaxBands;
+  int* mode = reinterpret_cast<int*>(hi + kMaxBands);
+  float* cover = reinterpret_cast<float*>(mode + kMaxBands);
+  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows,
+                                   (int)std::floor(rmin / (double)kRowStep), sec_lo, sec_hi, lo,
+                                   hi, mode, cover);
+  c->sh_cover = cover;
+  c->sh_lo = lo;
+  c->sh_hi = hi;
+  c->sh_mode = mode;
+  // directories sized for density (k_band_setup): up to ~4x the global count
+  CUDA_TRY(c->dir.ensure(4 * (size_t)((4 * n << kDirExtra) + 2 * kMaxBands + 64)));
+  CUDA_TRY(c->sh_keep.ensure((size_t)n));
+  k_shard_flags<<<blocks_for(n), 256, 0, st>>>(n, c->k32_in.as<uint32_t>(), lo, hi, mode,
+                                               c->sh_keep.as<uint8_t>());
+  // order-preserving compaction of (key, id) into the sort's output buffers,
+  // then back
+  int* d_cnt = reinterpret_cast<int*>(c->sh_buf.as<char>() + 960);
+  tb = 0;
+  CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tb, c->k32_in.as<uint32_t>(),
+                                      c->sh_keep.as<uint8_t>(), c->k32_out.as<uint32_t>(), d_cnt,
+                                      (int)n, st));
+  CUDA_TRY(c->temp.ensure(tb));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceSelect::Flagged(c->temp.p, tb, c->k32_in.as<uint32_t>(),
+                                      c->sh_keep.as<uint8_t>(), c->k32_out.as<uint32_t>(), d_cnt,
+                                      (int)n, st));
+  tb = c->temp.bytes;
+  CUDA_TRY(cub::DeviceSelect::Flagged(c->temp.p, tb, c->vals_in.as<int32_t>(),
+                                      c->sh_keep.as<uint8_t>(), c->vals_out.as<int32_t>(), d_cnt,
+                                      (int)n, st));
+  int np = 0;
+  CUDA_TRY(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaMemcpyAsync(c->k32_in.p, c->k32_out.p, 4 * (size_t)np, cudaMemcpyDeviceToDevice,
+                           st));
+  CUDA_TRY(cudaMemcpyAsync(c->vals_in.p, c->vals_out.p, 4 * (size_t)np, cudaMemcpyDeviceToDevice,
+                           st));
+  c->np = np;
+  return HRG_OK;
+}
+
 hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* shard,
                         bool sample_ids, bool from_coords, uint64_t seed, hrg_stats* stats) {
   int64_t n = M->n;
@@ -480,7 +580,13 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev[E_SAMPLED], st));
-  hrg_status s = build_index(c, M, S, L, shard, C, sample_ids);
+  c->np = n;
+  hrg_status s = HRG_OK;
+  if (shard && shard->count > 1 && sample_ids) {
+    s = shard_subset(c, M, S, L, shard);
+    if (s != HRG_OK) return s;
+  }
+  s = build_index(c, M, S, L, shard, C, sample_ids);
   if (s != HRG_OK) return s;
   if (stats) stats->kernel_launches = 7;  // sample/keys, gather, 5 index kernels (+ CUB sort)
   s = emit_edges(c, M, L, C, sample_ids, stats);
@@ -535,8 +641,9 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
-                 &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad,
-                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->widen})
+                 &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps,
+                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep,
+                 &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   delete c;

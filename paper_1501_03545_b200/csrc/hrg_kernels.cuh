@@ -260,7 +260,8 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n,
 // One block: band position ranges, shard query ranges, directory sizing.
 __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L,
                              uint64_t qsec_lo, uint64_t qsec_hi, Band* __restrict__ bands,
-                             int64_t* __restrict__ dir_total) {
+                             int64_t* __restrict__ dir_total,
+                             const float* __restrict__ cover) {
   __shared__ int64_t st[kMaxBands + 1];
   int j = threadIdx.x;
   if (j <= L) st[j] = lower_bound_u64(keys, n, (uint64_t)j << kQBits);
@@ -273,6 +274,9 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     B.qstart = (int32_t)lower_bound_u64(keys, n, base | qsec_lo);
     B.qend = qsec_hi > kQMask ? B.end : (int32_t)lower_bound_u64(keys, n, base | qsec_hi);
     int64_t cnt = B.end - B.start;
+    // a sharded run's subset covers only part of the circle: size the
+    // directory for the band's density, not its count
+    if (cover && cnt > 0) cnt = (int64_t)ceil((double)cnt / fmax((double)cover[j], 1e-6));
     int lg = 0;
     while ((1ll << lg) < cnt && lg < kQBits - kSortShift) ++lg;  // nb = next pow2 >= cnt
     lg = min(lg + kDirExtra, kQBits - kSortShift);                // (x 2^kDirExtra)
@@ -337,9 +341,21 @@ __global__ void k_band_finish(Band* bands, int L) {
 }
 
 // dir[base + k] = first position of the band whose bucket >= k.
+// dir[b] = first position of the band whose bucket is >= b: every point
+// fills the buckets between its predecessor's and its own.  Gaps longer than
+// kDirGapInline buckets (empty angular stretches: sparse inner bands, the
+// region outside a sharded run's sector) are queued for k_dir_gaps.
+constexpr int kDirGapInline = 64;
+struct DirGap {
+  int64_t begin, end;
+  int32_t value, pad;
+};
+
 __global__ void __launch_bounds__(256) k_dir_fill(int64_t n, const uint64_t* __restrict__ keys,
                                                   const Band* __restrict__ bands,
-                                                  int32_t* __restrict__ dir) {
+                                                  int32_t* __restrict__ dir,
+                                                  DirGap* __restrict__ gaps,
+                                                  unsigned* __restrict__ ngaps) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   uint64_t key = keys[p];
@@ -348,16 +364,65 @@ __global__ void __launch_bounds__(256) k_dir_fill(int64_t n, const uint64_t* __r
   int64_t b = (int64_t)((key & kQMask) >> B.shift);
   int64_t bprev = -1;
   if (p > B.start) bprev = (int64_t)((keys[p - 1] & kQMask) >> B.shift);
-  for (int64_t k = bprev + 1; k <= b; ++k) dir[B.dir_base + k] = (int32_t)p;
+  if (b - bprev <= kDirGapInline) {
+    for (int64_t k = bprev + 1; k <= b; ++k) dir[B.dir_base + k] = (int32_t)p;
+  } else {
+    const unsigned g = atomicAdd(ngaps, 1u);
+    gaps[g].begin = bprev + 1;
+    gaps[g].end = b + 1;
+    gaps[g].value = (int32_t)p;
+    gaps[g].pad = j;
+  }
+}
+
+// Sharded subset: only the buckets of a band's needed range (+1 either side,
+// circular) are ever looked up; the rest of a gap is left unwritten.
+struct ShardRanges {
+  const int64_t* lo;  // 27-bit key units, see k_shard_ranges
+  const int64_t* hi;
+  const int* mode;    // -1 none, 0 [lo, hi), 1 whole band
+};
+
+__device__ __forceinline__ void fill_range(int32_t* dir, const Band& B, int64_t b0, int64_t b1,
+                                           int32_t value, const ShardRanges* R, int j, int t0,
+                                           int nt) {
+  if (R && R->mode[j] == 0) {
+    const int64_t bl = ((R->lo[j] << kSortShift) >> B.shift) - 1;
+    const int64_t bh = ((R->hi[j] << kSortShift) >> B.shift) + 2;
+    int64_t lo[2], hi[2];
+    int m = 0;
+    if (R->lo[j] <= R->hi[j]) { lo[0] = bl; hi[0] = bh; m = 1; }
+    else { lo[0] = bl; hi[0] = B.nb + 1; lo[1] = 0; hi[1] = bh; m = 2; }
+    for (int r = 0; r < m; ++r) {
+      const int64_t a = max(b0, lo[r]), e = min(b1, hi[r]);
+      for (int64_t k = a + t0; k < e; k += nt) dir[B.dir_base + k] = value;
+    }
+  } else {
+    for (int64_t k = b0 + t0; k < b1; k += nt) dir[B.dir_base + k] = value;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dir_gaps(const DirGap* __restrict__ gaps,
+                                                  const unsigned* __restrict__ ngaps,
+                                                  const Band* __restrict__ bands,
+                                                  int32_t* __restrict__ dir, ShardRanges R,
+                                                  bool sharded) {
+  const unsigned ng = *ngaps;
+  for (unsigned g = blockIdx.x; g < ng; g += gridDim.x) {
+    const DirGap G = gaps[g];
+    const Band B = bands[G.pad];
+    fill_range(dir, B, G.begin, G.end, G.value, sharded ? &R : nullptr, G.pad, threadIdx.x,
+               blockDim.x);
+  }
 }
 
 __global__ void k_dir_tail(const uint64_t* __restrict__ keys, const Band* __restrict__ bands,
-                           int32_t* __restrict__ dir) {
+                           int32_t* __restrict__ dir, ShardRanges R, bool sharded) {
   Band B = bands[blockIdx.x];
   int64_t last = -1;
   if (B.end > B.start) last = (int64_t)((keys[B.end - 1] & kQMask) >> B.shift);
-  for (int64_t k = last + 1 + threadIdx.x; k <= B.nb; k += blockDim.x)
-    dir[B.dir_base + k] = B.end;
+  fill_range(dir, B, last + 1, (int64_t)B.nb + 1, B.end, sharded ? &R : nullptr, blockIdx.x,
+             threadIdx.x, blockDim.x);
 }
 
 constexpr int kLightMax = 2048;    // queries with more candidates take the heavy path
@@ -495,6 +560,46 @@ __global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, 
     out = d < 0.0 ? -1.0f : (d >= 3.14159 ? 4.0f : __double2float_ru(d * 1.01));
   }
   wtab[s * L + j] = out;
+}
+
+// Sharded runs: the angular range of each band that any query of this
+// rank's sector can reach.  wtab was built on bands whose innermost radius is
+// the band's threshold (a lower bound, so windows only widen); windows shrink
+// with the query radius, so rows from the smallest query radius on bound
+// every query.  Output per band, in 27-bit sort-key units: [lo, hi) of
+// needed keys (circular; lo > hi wraps), or whole = 1, or none = -1.
+__global__ void k_shard_ranges(const float* __restrict__ wtab, int L, int rows, int s0,
+                               int64_t sec_lo, int64_t sec_hi, int64_t* __restrict__ lo,
+                               int64_t* __restrict__ hi, int* __restrict__ mode,
+                               float* __restrict__ cover) {
+  const int j = threadIdx.x;
+  if (j >= L) return;
+  float d = -1.0f;
+  for (int s = max(s0, 0); s < rows; ++s) d = fmaxf(d, wtab[s * L + j]);
+  const int64_t span = (int64_t)1 << 27;
+  cover[j] = 1.0f;
+  if (d < 0.0f) { mode[j] = -1; return; }
+  const double w = (double)d * (double)span / kTwoPi;
+  const int64_t dk = (int64_t)ceil(w * (1.0 + 1e-9)) + 2;
+  if (d >= 3.14159f || 2 * dk + (sec_hi - sec_lo) >= span) { mode[j] = 1; return; }
+  mode[j] = 0;
+  lo[j] = ((sec_lo - dk) % span + span) % span;
+  hi[j] = (sec_hi + dk) % span;
+  cover[j] = (float)((double)(2 * dk + (sec_hi - sec_lo)) / (double)span);
+}
+
+__global__ void k_shard_flags(int64_t n, const uint32_t* __restrict__ k32,
+                              const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+                              const int* __restrict__ mode, uint8_t* __restrict__ keep) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = k32[i];
+  const int b = (int)(k >> 27);
+  const int64_t q = (int64_t)(k & ((1u << 27) - 1));
+  const int md = mode[b];
+  bool ok = md > 0;
+  if (md == 0) ok = lo[b] <= hi[b] ? (q >= lo[b] && q < hi[b]) : (q >= lo[b] || q < hi[b]);
+  keep[i] = ok ? 1 : 0;
 }
 
 // Window of band B for a query at angle phi with table half-width dlt, as
