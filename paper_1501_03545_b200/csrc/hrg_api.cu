@@ -94,6 +94,8 @@ struct hrg_context {
   const int* sh_mode = nullptr;
   bool have_result = false;
   bool coords_sorted = false;  // angular order: coordinates live in s_phi/s_rn/s_rp
+  bool coords_pending = false; // sample order: phi/rn/rp not yet materialised
+  SampleParams pending{};
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
@@ -473,12 +475,10 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   cudaStream_t st = c->stream;
   // smallest Poincare radius present (the widest windows)
   CUDA_TRY(c->sh_buf.ensure(1024));
-  double* d_min = reinterpret_cast<double*>(c->sh_buf.p);
+  unsigned long long* d_min = reinterpret_cast<unsigned long long*>(c->sh_buf.p);
+  CUDA_TRY(cudaMemsetAsync(d_min, 0xff, 8, st));
+  k_min_rp<<<4 * c->sm_count, 256, 0, st>>>(n, c->pr.as<double2>(), d_min);
   size_t tb = 0;
-  CUDA_TRY(cub::DeviceReduce::Min(nullptr, tb, c->rp.as<double>(), d_min, (int)n, st));
-  CUDA_TRY(c->temp.ensure(tb));
-  tb = c->temp.bytes;
-  CUDA_TRY(cub::DeviceReduce::Min(c->temp.p, tb, c->rp.as<double>(), d_min, (int)n, st));
   double pmin = 0.0;
   CUDA_TRY(cudaMemcpyAsync(&pmin, d_min, 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -564,10 +564,16 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   CUDA_TRY(cudaEventRecord(c->ev[E_START], st));
   if (!from_coords) {
     SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
-    k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
-                                            c->rp.as<double>(), c->k32_in.as<uint32_t>(),
-                                            c->vals_in.as<int32_t>(), c->pr.as<double2>());
+    // coordinates on request only (hrg_result_device_ptrs); angular order
+    // gathers r_native into its sorted copy, so that one is written
+    k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, nullptr,
+                                            sample_ids ? nullptr : c->rn.as<double>(), nullptr,
+                                            c->k32_in.as<uint32_t>(), c->vals_in.as<int32_t>(),
+                                            c->pr.as<double2>());
+    c->coords_pending = sample_ids;
+    c->pending = P;
   } else {
+    c->coords_pending = false;
     CUDA_TRY(cudaMemsetAsync(c->bad.p, 0, 4, st));
     k_keys_from_coords<<<blocks_for(n), 256, 0, st>>>(
         n, c->phi.as<double>(), c->rp.as<double>(), M->max_r, C, S, c->rn.as<double>(),
@@ -794,6 +800,13 @@ hrg_status hrg_result_device_ptrs(hrg_context* c, const double** phi, const doub
                                   const double** rp, const int64_t** indptr,
                                   const int32_t** indices) {
   if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
+  if ((phi || rn || rp) && c->coords_pending) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    k_sample_coords<<<blocks_for(c->n), 256, 0, c->stream>>>(
+        c->n, c->pending, c->phi.as<double>(), c->rn.as<double>(), c->rp.as<double>());
+    CUDA_TRY(cudaGetLastError());
+    c->coords_pending = false;
+  }
   if (phi) *phi = c->coords_sorted ? c->s_phi.as<double>() : c->phi.as<double>();
   if (rn) *rn = c->coords_sorted ? c->s_rn.as<double>() : c->rn.as<double>();
   if (rp) *rp = c->coords_sorted ? c->s_rp.as<double>() : c->rp.as<double>();
@@ -811,8 +824,10 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
   cudaStream_t st = c->stream;
   cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   size_t d = sizeof(double) * (size_t)c->n;
-  const double *sp, *sn, *sr;
-  hrg_result_device_ptrs(c, &sp, &sn, &sr, nullptr, nullptr);
+  const double *sp = nullptr, *sn = nullptr, *sr = nullptr;
+  hrg_status s = hrg_result_device_ptrs(c, phi ? &sp : nullptr, rn ? &sn : nullptr,
+                                        rp ? &sr : nullptr, nullptr, nullptr);
+  if (s != HRG_OK) return s;
   if (phi) CUDA_TRY(cudaMemcpyAsync(phi, sp, d, k, st));
   if (rn) CUDA_TRY(cudaMemcpyAsync(rn, sn, d, k, st));
   if (rp) CUDA_TRY(cudaMemcpyAsync(rp, sr, d, k, st));

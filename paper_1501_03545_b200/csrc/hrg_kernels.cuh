@@ -128,6 +128,22 @@ __device__ __forceinline__ uint32_t sort_key32(int band, uint64_t q) {
 // hrgen generator.py:160-179 with a counter-based stream: vertex i draws its
 // angle from the first and its radius from the second 53-bit uniform of
 // Philox4x32-10(counter = i, key = seed).
+__device__ __forceinline__ void sample_point(int64_t i, const SampleParams& P, double& ph,
+                                             double& r, double& p) {
+  uint32_t c[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 0u, 0u};
+  philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
+  uint64_t a = (((uint64_t)c[1] << 32) | c[0]) >> 11;
+  uint64_t b = (((uint64_t)c[3] << 32) | c[2]) >> 11;
+  double u1 = (double)a * 0x1.0p-53, u2 = (double)b * 0x1.0p-53;
+  ph = __dmul_rn(kTwoPi, u1);                                          // :170
+  r = __dmul_rn(P.two_over_alpha, asinh(__dmul_rn(__dsqrt_rn(u2), P.sinh_half)));
+  r = fmin(r, P.r_cap);                                                // :174
+  p = fmin(tanh(__dmul_rn(r, 0.5)), P.rp_cap);                        // :175-178
+}
+
+// The pipeline's sampler: packed (phi, r_p), sort key and id per vertex; the
+// API's coordinate arrays only when asked for (a generation materialises
+// them later, on request, with k_sample_coords -- same stream, same bits).
 __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandSpec S,
                                                 double* __restrict__ phi, double* __restrict__ rn,
                                                 double* __restrict__ rp,
@@ -136,19 +152,37 @@ __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandS
                                                 double2* __restrict__ pr) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint32_t c[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 0u, 0u};
-  philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
-  uint64_t a = (((uint64_t)c[1] << 32) | c[0]) >> 11;
-  uint64_t b = (((uint64_t)c[3] << 32) | c[2]) >> 11;
-  double u1 = (double)a * 0x1.0p-53, u2 = (double)b * 0x1.0p-53;
-  double ph = __dmul_rn(kTwoPi, u1);                                   // :170
-  double r = __dmul_rn(P.two_over_alpha, asinh(__dmul_rn(__dsqrt_rn(u2), P.sinh_half)));
-  r = fmin(r, P.r_cap);                                                // :174
-  double p = fmin(tanh(__dmul_rn(r, 0.5)), P.rp_cap);                 // :175-178
-  phi[i] = ph; rn[i] = r; rp[i] = p;
+  double ph, r, p;
+  sample_point(i, P, ph, r, p);
+  if (phi) phi[i] = ph;
+  if (rn) rn[i] = r;
+  if (rp) rp[i] = p;
   pr[i] = make_double2(ph, p);
   keys[i] = sort_key32(band_of(S, p), qkey(ph, P.C));
   vals[i] = (int32_t)i;
+}
+
+__global__ void __launch_bounds__(256) k_sample_coords(int64_t n, SampleParams P,
+                                                       double* __restrict__ phi,
+                                                       double* __restrict__ rn,
+                                                       double* __restrict__ rp) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ph, r, p;
+  sample_point(i, P, ph, r, p);
+  phi[i] = ph; rn[i] = r; rp[i] = p;
+}
+
+// smallest Poincare radius (positive doubles order like their bit patterns)
+__global__ void __launch_bounds__(256) k_min_rp(int64_t n, const double2* __restrict__ pr,
+                                                unsigned long long* __restrict__ out) {
+  unsigned long long m = ~0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = min(m, (unsigned long long)__double_as_longlong(pr[i].y));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(out, m);
 }
 
 // Keys for caller-supplied coordinates; flags points outside the tree region
