@@ -261,6 +261,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   A.C = C;
   A.bump = c->counters.as<unsigned long long>();
   A.cand_total = c->counters.as<unsigned long long>() + 1;
+  A.tile_next = c->counters.as<unsigned long long>() + 11;
   A.heavy_n = reinterpret_cast<unsigned*>(c->counters.as<unsigned long long>() + 2);
   A.overflow = reinterpret_cast<int*>(c->counters.as<unsigned long long>() + 3);
   A.stage_off = c->stage_off.as<int64_t>();
