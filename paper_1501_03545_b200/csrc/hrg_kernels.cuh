@@ -498,7 +498,7 @@ struct QueryArgs {
   // ~0 = no tile)
   const uint64_t* tiles;
   int64_t ntiles;            // entries (an upper bound on the tiles)
-  unsigned long long* tile_next;  // k_light's dynamic tile counter
+  unsigned long long* tile_next;  // dynamic tile counters: k_light, k_compact_light
 };
 
 // Tile table: every band's query range cut into tiles of 32 positions (the
@@ -1410,7 +1410,10 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
   int32_t* sm = buf[threadIdx.x >> 5];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t tk = wid; tk < A.ntiles; tk += nw) {
+  int64_t tk = wid;
+  for (; tk < A.ntiles;
+       tk = __shfl_sync(FULL, lane == 0 ? (int64_t)(nw + atomicAdd(A.tile_next + 1, 1ull)) : 0,
+                        0)) {
     const uint64_t tv = __ldg(A.tiles + tk);
     if (tv == ~0ull) break;
     const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
