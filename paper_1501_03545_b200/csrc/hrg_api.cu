@@ -299,6 +299,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   if (c->grid_light == 0) {
     c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
+    // (k_compact_heavy shares the heavy grid: both walk the chunk list)
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSortWarpSmem));
@@ -314,56 +315,122 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   unsigned gc = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
-  // generous estimate; an overflow is detected and the pass re-run
+  // generous estimate.  Everything after the light pass runs without a host
+  // round trip (buffers sized by upper bounds, counts read on the device);
+  // one synchronisation at the end checks for a staging overflow, in which
+  // case the pass is re-run with the capacity the bump allocator reached.
   if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * np, 1 << 20);
-  int64_t H = 0, total_chunks = 0, nnz = 0;
-  unsigned long long ctr[8];
+  unsigned long long ctr[16];
+  int64_t nnz = 0, total_chunks = 0;
   for (int attempt = 0; attempt < 3; ++attempt) {
-    CUDA_TRY(c->stage.ensure(4 * (size_t)c->stage_cap));
+    const int64_t cap = c->stage_cap;  // also bounds hits, chunks, rows to sort
+    CUDA_TRY(c->stage.ensure(4 * (size_t)cap));
     A.stage = c->stage.as<int32_t>();
-    A.stage_cap = c->stage_cap;
+    A.stage_cap = cap;
+    const int64_t hcap = np + 1;                     // deferred queries
+    const int64_t ccap = cap / kChunk + np + 1;      // their chunks
+    CUDA_TRY(c->nchunks.ensure(4 * (size_t)hcap));
+    CUDA_TRY(c->chunk_start.ensure(8 * (size_t)(hcap + 1)));
+    CUDA_TRY(c->chunk_hits.ensure(4 * (size_t)ccap));
+    CUDA_TRY(c->chunk_entry.ensure(4 * (size_t)ccap));
+    CUDA_TRY(c->chunk_off.ensure(8 * (size_t)(ccap + 1)));
+    CUDA_TRY(c->idx.ensure(4 * (size_t)cap));
+    unsigned long long* ctrs = c->counters.as<unsigned long long>();
+    int64_t* d_chunks = reinterpret_cast<int64_t*>(ctrs + 14);  // 11, 12: tile counters
+    A.chunk_start = c->chunk_start.as<int64_t>();
+    A.chunk_entry = c->chunk_entry.as<int32_t>();
+    A.chunk_hits = c->chunk_hits.as<int32_t>();
+    A.total_chunks = d_chunks;
+
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
     else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
-    launches++;
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    H = (int64_t)(ctr[2] & 0xffffffffull);
-    total_chunks = 0;
-    if (H > 0) {
-      CUDA_TRY(c->nchunks.ensure(4 * (size_t)H));
-      CUDA_TRY(c->chunk_start.ensure(8 * (size_t)(H + 1)));
-      k_heavy_chunks<<<blocks_for(H), 256, 0, st>>>(A.heavy_c, H, c->nchunks.as<int32_t>());
-      hrg_status s = scan_i32_to_i64(c, c->nchunks.as<int32_t>(), c->chunk_start.as<int64_t>(), H);
-      if (s != HRG_OK) return s;
-      CUDA_TRY(cudaMemcpyAsync(&total_chunks, c->chunk_start.as<int64_t>() + H, 8,
-                               cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      CUDA_TRY(c->chunk_hits.ensure(4 * (size_t)total_chunks));
-      CUDA_TRY(c->chunk_entry.ensure(4 * (size_t)total_chunks));
-      k_chunk_owner<<<blocks_for(H), 256, 0, st>>>(c->chunk_start.as<int64_t>(), H,
-                                                   c->chunk_entry.as<int32_t>());
-      A.chunk_entry = c->chunk_entry.as<int32_t>();
-      A.chunk_start = c->chunk_start.as<int64_t>();
-      A.chunk_hits = c->chunk_hits.as<int32_t>();
-      A.total_chunks = total_chunks;
-      unsigned gh = (unsigned)std::max<int64_t>(
-          1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
-      if (sample_ids) k_heavy<true><<<gh, 256, 0, st>>>(A, H);
-      else k_heavy<false><<<gh, 256, 0, st>>>(A, H);
-      launches += 3;
-    }
+    k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),
+                                     c->chunk_start.as<int64_t>(), c->chunk_entry.as<int32_t>(),
+                                     d_chunks, A.overflow);
+    if (sample_ids) k_heavy<true><<<c->grid_heavy, 256, 0, st>>>(A, 0);
+    else k_heavy<false><<<c->grid_heavy, 256, 0, st>>>(A, 0);
     CUDA_TRY(cudaEventRecord(c->ev[E_COUNTED], st));
     CUDA_TRY(cudaGetLastError());
     hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
     if (s != HRG_OK) return s;
+
+    int32_t* idx = c->idx.as<int32_t>();
+    const int64_t* rp = c->rowptr.as<int64_t>();
+    // sort jobs (sample order): light rows above kSmallSlots ids, heavy rows
+    const int64_t jcap = 2 * np + 1;
+    const int64_t mcap = cap / (kWarpBucketMax + 1) + 1;
+    const int64_t lcap = cap / (kBucketMax + 1) + 1;
+    CUDA_TRY(c->job_dst.ensure(8 * (size_t)jcap));
+    CUDA_TRY(c->job_len.ensure(4 * (size_t)jcap));
+    CUDA_TRY(c->mid_off.ensure(8 * (size_t)mcap));
+    CUDA_TRY(c->mid_len.ensure(4 * (size_t)mcap));
+    CUDA_TRY(c->large_off.ensure(8 * (size_t)lcap));
+    CUDA_TRY(c->large_len.ensure(4 * (size_t)lcap));
+    const int64_t gcap = cap / (kLargeMax + 1) + 1;          // giant rows
+    const int64_t bcap = cap / kGiantTarget + gcap + 1;      // their sub-buckets / chunks
+    CUDA_TRY(c->giant_off.ensure(8 * (size_t)gcap));
+    CUDA_TRY(c->giant_len.ensure(4 * (size_t)gcap));
+    CUDA_TRY(c->giant_meta.ensure(4 * 3 * (size_t)gcap));
+    CUDA_TRY(c->sub_off.ensure(8 * (size_t)bcap));
+    CUDA_TRY(c->sub_len.ensure(4 * (size_t)bcap));
+    CUDA_TRY(c->sub_cur.ensure(8 * (size_t)bcap));
+    CUDA_TRY(c->chunk_row.ensure(4 * (size_t)bcap));
+    SortJobs J;
+    J.rows = RowList{c->job_dst.as<int64_t>(), c->job_len.as<int32_t>(),
+                     reinterpret_cast<unsigned*>(ctrs + 4)};
+    J.mid = RowList{c->mid_off.as<int64_t>(), c->mid_len.as<int32_t>(),
+                    reinterpret_cast<unsigned*>(ctrs + 5)};
+    unsigned* uctr = reinterpret_cast<unsigned*>(ctrs + 6);  // 4 more 32-bit counters
+    J.large = RowList{c->large_off.as<int64_t>(), c->large_len.as<int32_t>(), uctr};
+    Giant G;
+    G.rows = RowList{c->giant_off.as<int64_t>(), c->giant_len.as<int32_t>(), uctr + 1};
+    G.sub = RowList{c->sub_off.as<int64_t>(), c->sub_len.as<int32_t>(), uctr + 2};
+    G.nchunks = uctr + 3;
+    G.nb = c->giant_meta.as<int32_t>();
+    G.bbase = G.nb + gcap;
+    G.cbase = G.nb + 2 * gcap;
+    G.chunk_row = c->chunk_row.as<int32_t>();
+    G.cur = c->sub_cur.as<unsigned long long>();
+    CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
+    if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
+    else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
+    k_scan_chunks<<<1, 1024, 0, st>>>(c->chunk_hits.as<int32_t>(), d_chunks,
+                                      c->chunk_off.as<int64_t>(), A.overflow);
+    k_compact_heavy<<<c->grid_heavy, 256, 0, st>>>(A, 0, c->chunk_off.as<int64_t>(), rp, idx,
+                                                   sample_ids);
+    if (sample_ids) k_queue_heavy_rows<<<2 * c->sm_count, 256, 0, st>>>(A, rp, J);
+    CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
+    c->idx_final = idx;
+    if (sample_ids) {
+      // rows by length: a warp (<= kWarpBucketMax), a 256-thread block
+      // (<= kBucketMax), a 1024-thread block (<= kLargeMax); giant (hub) rows
+      // are first split by value into sub-buckets through the scratch array
+      CUDA_TRY(c->idx2.ensure(4 * (size_t)cap));
+      const RowList none{nullptr, nullptr, nullptr};
+      const unsigned sm = (unsigned)c->sm_count;
+      k_sort_warp<<<8 * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
+      k_sort_rows<256, kBucketMax, kMidShift>
+          <<<8 * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(idx, idx, J.mid, J.large);
+      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+          idx, idx, J.large, G.rows);
+      k_giant_plan<<<1, 1024, 0, st>>>(G);
+      k_giant_hist<<<2 * sm, 1024, 0, st>>>(idx, G, n);
+      k_giant_scan<<<sm, 1024, 0, st>>>(G);
+      k_giant_scatter<<<2 * sm, 1024, 0, st>>>(idx, c->idx2.as<int32_t>(), G, n);
+      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+          c->idx2.as<int32_t>(), idx, G.sub, none);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
+    CUDA_TRY(cudaGetLastError());
+    // the one synchronisation: counters, edge total, overflow flag
+    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 128, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 64, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    total_chunks = (int64_t)ctr[14];
     if ((ctr[3] & 0xffffffffull) == 0) break;
     // staging overflowed: size it from the bump allocator's final value
     c->stage_cap = (int64_t)(ctr[0] + ctr[0] / 8 + 4096);
@@ -371,94 +438,13 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   }
   // next call: keep ~10% headroom over this call's staging use
   c->stage_cap = std::max<int64_t>(c->stage_cap, (int64_t)(ctr[0] + ctr[0] / 10 + 4096));
-
-  CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
-  int32_t* idx = c->idx.as<int32_t>();
-  const int64_t* rp = c->rowptr.as<int64_t>();
-  // sort jobs (sample order): light rows above kSmallSlots ids, heavy rows
-  const int64_t jcap = np + H + 1;
-  const int64_t mcap = nnz / (kWarpBucketMax + 1) + 1;
-  const int64_t lcap = nnz / (kBucketMax + 1) + 1;
-  CUDA_TRY(c->job_dst.ensure(8 * (size_t)jcap));
-  CUDA_TRY(c->job_len.ensure(4 * (size_t)jcap));
-  CUDA_TRY(c->mid_off.ensure(8 * (size_t)mcap));
-  CUDA_TRY(c->mid_len.ensure(4 * (size_t)mcap));
-  CUDA_TRY(c->large_off.ensure(8 * (size_t)lcap));
-  CUDA_TRY(c->large_len.ensure(4 * (size_t)lcap));
-  const int64_t gcap = nnz / (kLargeMax + 1) + 1;          // giant rows
-  const int64_t bcap = nnz / kGiantTarget + gcap + 1;      // their sub-buckets / chunks
-  CUDA_TRY(c->giant_off.ensure(8 * (size_t)gcap));
-  CUDA_TRY(c->giant_len.ensure(4 * (size_t)gcap));
-  CUDA_TRY(c->giant_meta.ensure(4 * 3 * (size_t)gcap));
-  CUDA_TRY(c->sub_off.ensure(8 * (size_t)bcap));
-  CUDA_TRY(c->sub_len.ensure(4 * (size_t)bcap));
-  CUDA_TRY(c->sub_cur.ensure(8 * (size_t)bcap));
-  CUDA_TRY(c->chunk_row.ensure(4 * (size_t)bcap));
-  unsigned long long* ctrs = c->counters.as<unsigned long long>();
-  SortJobs J;
-  J.rows = RowList{c->job_dst.as<int64_t>(), c->job_len.as<int32_t>(),
-                   reinterpret_cast<unsigned*>(ctrs + 4)};
-  J.mid = RowList{c->mid_off.as<int64_t>(), c->mid_len.as<int32_t>(),
-                  reinterpret_cast<unsigned*>(ctrs + 5)};
-  unsigned* uctr = reinterpret_cast<unsigned*>(ctrs + 6);  // 4 more 32-bit counters
-  J.large = RowList{c->large_off.as<int64_t>(), c->large_len.as<int32_t>(), uctr};
-  Giant G;
-  G.rows = RowList{c->giant_off.as<int64_t>(), c->giant_len.as<int32_t>(), uctr + 1};
-  G.sub = RowList{c->sub_off.as<int64_t>(), c->sub_len.as<int32_t>(), uctr + 2};
-  G.nchunks = uctr + 3;
-  G.nb = c->giant_meta.as<int32_t>();
-  G.bbase = G.nb + gcap;
-  G.cbase = G.nb + 2 * gcap;
-  G.chunk_row = c->chunk_row.as<int32_t>();
-  G.cur = c->sub_cur.as<unsigned long long>();
-  CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
-  if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
-  else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
-  launches++;
-  if (total_chunks > 0) {
-    CUDA_TRY(c->chunk_off.ensure(8 * (size_t)(total_chunks + 1)));
-    hrg_status s = scan_i32_to_i64(c, c->chunk_hits.as<int32_t>(), c->chunk_off.as<int64_t>(),
-                                   total_chunks);
-    if (s != HRG_OK) return s;
-    unsigned gh = (unsigned)std::max<int64_t>(
-        1, std::min<int64_t>((total_chunks * 32 + 255) / 256, c->grid_heavy));
-    k_compact_heavy<<<gh, 256, 0, st>>>(A, H, c->chunk_off.as<int64_t>(), rp, idx, sample_ids);
-    launches++;
-    if (sample_ids) {
-      k_queue_heavy_rows<<<blocks_for(H), 256, 0, st>>>(A, H, rp, J);
-      launches++;
-    }
-  }
-  CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
-  c->idx_final = idx;
-  if (sample_ids) {
-    // rows by length: a warp (<= kWarpBucketMax), a 256-thread block
-    // (<= kBucketMax), a 1024-thread block (<= kLargeMax); giant (hub) rows
-    // are first split by value into sub-buckets through the scratch array
-    CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
-    const RowList none{nullptr, nullptr, nullptr};
-    const unsigned sm = (unsigned)c->sm_count;
-    k_sort_warp<<<8 * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
-    k_sort_rows<256, kBucketMax, kMidShift><<<8 * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(
-        idx, idx, J.mid, J.large);
-    k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
-        idx, idx, J.large, G.rows);
-    k_giant_plan<<<1, 1024, 0, st>>>(G);
-    k_giant_hist<<<2 * sm, 1024, 0, st>>>(idx, G, n);
-    k_giant_scan<<<sm, 1024, 0, st>>>(G);
-    k_giant_scatter<<<2 * sm, 1024, 0, st>>>(idx, c->idx2.as<int32_t>(), G, n);
-    k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
-        c->idx2.as<int32_t>(), idx, G.sub, none);
-    launches += 8;
-    CUDA_TRY(cudaGetLastError());
-  }
-  CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
+  launches += 9 + (sample_ids ? 9 : 0);  // light, heavy prep+pass, 3 scans, compaction(s), sorts
   c->nnz = nnz;
   if (stats) {
     stats->nnz = nnz;
     stats->m = nnz / 2;
     stats->candidates = (int64_t)ctr[1];
-    stats->heavy_queries = H;
+    stats->heavy_queries = (int64_t)(ctr[2] & 0xffffffffull);
     stats->heavy_chunks = total_chunks;
     stats->kernel_launches += launches;
   }

@@ -490,7 +490,7 @@ struct QueryArgs {
   int32_t* heavy_of;         // sorted position -> entry, or -1
   const int64_t* chunk_start;// entry -> first chunk (exclusive scan, H + 1)
   const int32_t* chunk_entry;// chunk -> entry
-  int64_t total_chunks;
+  const int64_t* total_chunks;  // device scalar (k_heavy_prep)
   int32_t* chunk_hits;
   int32_t* deg;              // row length per vertex id
   unsigned long long* cand_total;
@@ -1115,18 +1115,76 @@ __global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(Qu
   if (lane == 0 && cand_local) atomicAdd(A.cand_total, cand_local);
 }
 
-// chunk -> heavy entry (the inverse of chunk_start)
-__global__ void k_chunk_owner(const int64_t* __restrict__ chunk_start, int64_t H,
-                              int32_t* __restrict__ chunk_entry) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= H) return;
-  for (int64_t c = chunk_start[e]; c < chunk_start[e + 1]; ++c) chunk_entry[c] = (int32_t)e;
+// Exclusive scan of a device-sized int32 array into int64 out[0, count],
+// one block (the counts here are the deferred queries' chunks: small).
+__device__ void block_scan_i64(const int32_t* in, int64_t count, int64_t* out) {
+  __shared__ int64_t s_w[32];
+  __shared__ int64_t s_run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < count; b0 += blockDim.x) {
+    const int64_t i = b0 + tid;
+    const int64_t x = i < count ? (int64_t)in[i] : 0;
+    int64_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+      int64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      if (lane < (int)(blockDim.x >> 5)) s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    const int64_t ex = s_run + s_w[warp] + inc - x;
+    if (i < count) out[i] = ex;
+    __syncthreads();
+    if (tid == blockDim.x - 1) s_run = ex + x;
+    __syncthreads();
+  }
+  if (tid == 0) out[count] = s_run;
 }
 
-__global__ void k_heavy_chunks(const int32_t* __restrict__ heavy_c, int64_t H,
-                               int32_t* __restrict__ nchunks) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < H) nchunks[e] = (heavy_c[e] + kChunk - 1) / kChunk;
+// Deferred (heavy) queries, on the device so no host round trip sits between
+// the light pass and the heavy one: chunks per query, their exclusive scan
+// (chunk_start, total), and the chunk -> query map.
+__global__ void __launch_bounds__(1024) k_heavy_prep(const int32_t* __restrict__ heavy_c,
+                                                     const unsigned* __restrict__ heavy_n,
+                                                     int32_t* __restrict__ nchunks,
+                                                     int64_t* __restrict__ chunk_start,
+                                                     int32_t* __restrict__ chunk_entry,
+                                                     int64_t* __restrict__ total,
+                                                     const int* __restrict__ overflow) {
+  // a staging overflow voids the pass (re-run by the host); nothing after
+  // the light pass may then touch buffers sized by the staging capacity
+  if (*overflow) { if (threadIdx.x == 0) *total = 0; return; }
+  const int64_t H = *heavy_n;
+  for (int64_t e = threadIdx.x; e < H; e += blockDim.x)
+    nchunks[e] = (heavy_c[e] + kChunk - 1) / kChunk;
+  __syncthreads();
+  block_scan_i64(nchunks, H, chunk_start);
+  __syncthreads();
+  if (threadIdx.x == 0) *total = chunk_start[H];
+  for (int64_t e = threadIdx.x; e < H; e += blockDim.x)
+    for (int64_t c = chunk_start[e]; c < chunk_start[e + 1]; ++c) chunk_entry[c] = (int32_t)e;
+}
+
+// Exclusive scan of the heavy chunks' hit counts (count on the device).
+__global__ void __launch_bounds__(1024) k_scan_chunks(const int32_t* __restrict__ in,
+                                                      const int64_t* __restrict__ count,
+                                                      int64_t* __restrict__ out,
+                                                      const int* __restrict__ overflow) {
+  if (*overflow) return;
+  block_scan_i64(in, *count, out);
 }
 
 // Heavy pass: one warp per chunk of kChunk candidates of one deferred query;
@@ -1135,6 +1193,7 @@ __global__ void k_heavy_chunks(const int32_t* __restrict__ heavy_c, int64_t H,
 // chunk's slot of the query's staging slice.
 template <bool kSampleIds>
 __global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
+  if (*A.overflow) return;  // void pass, re-run by the host
   __shared__ Band sb[kMaxBands];
   if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
   __syncthreads();
@@ -1142,7 +1201,8 @@ __global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
+  const int64_t total_chunks = *A.total_chunks;
+  for (int64_t c = warp; c < total_chunks; c += nwarps) {
     const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
     const int64_t local = c - A.chunk_start[e];
@@ -1402,6 +1462,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <bool kSampleIds>
 __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_light(
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
+  if (*A.overflow) return;  // void pass, re-run by the host
   __shared__ Band sb[kMaxBands];
   __shared__ int32_t buf[kCompactThreads / 32][kTileHits];
   load_bands(A, sb);
@@ -2056,10 +2117,12 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
                                                        const int64_t* __restrict__ rowptr,
                                                        int32_t* __restrict__ idx,
                                                        bool sample_ids) {
+  if (*A.overflow) return;  // void pass, re-run by the host
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = warp; c < A.total_chunks; c += nwarps) {
+  const int64_t total_chunks = *A.total_chunks;
+  for (int64_t c = warp; c < total_chunks; c += nwarps) {
     const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
     const int32_t idv = sample_ids ? __ldg(A.rec.ids + v) : v;
@@ -2085,17 +2148,22 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
 
 // Sample-order ids: heavy rows arrive in (band, angle) order of their
 // neighbours; queue each for an in-place sort.
-__global__ void k_queue_heavy_rows(QueryArgs A, int64_t H, const int64_t* __restrict__ rowptr,
+__global__ void k_queue_heavy_rows(QueryArgs A, const int64_t* __restrict__ rowptr,
                                    SortJobs J) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t b = 0;
-  int32_t len = 0;
-  if (e < H) {
-    const int32_t idv = __ldg(A.rec.ids + A.heavy_v[e]);
-    b = rowptr[idv];
-    len = (int32_t)(rowptr[idv + 1] - b);
+  if (*A.overflow) return;  // void pass, re-run by the host
+  const int64_t H = *A.heavy_n;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x; e0 < H;
+       e0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e0 + threadIdx.x;
+    int64_t b = 0;
+    int32_t len = 0;
+    if (e < H) {
+      const int32_t idv = __ldg(A.rec.ids + A.heavy_v[e]);
+      b = rowptr[idv];
+      len = (int32_t)(rowptr[idv + 1] - b);
+    }
+    push_job_warp(J, len > 1, b, len);
   }
-  push_job_warp(J, len > 1, b, len);
 }
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,

@@ -326,3 +326,16 @@ def test_hub_rows_any_id_order(oracle, order):
     e, m, _ = oracle.edges_quadtree(phi, rp, a, alpha, max_r, 512, oracle.TRIG_CR)
     assert g.m == m
     assert edge_set_hash(oracle, g) == oracle.edge_hash(e)
+
+
+def test_staging_regrowth_after_small_graph():
+    """The staging buffer is sized from the previous call on a context; a
+    much larger graph right after a tiny one overflows it, the pass is voided
+    on the device and re-run, and the result equals a warm run's."""
+    eng = P.get_engine()
+    P.generate(GeneratorParams(n=2_000, avg_degree=6.0, gamma=3.0, seed=5))
+    p = GeneratorParams(n=400_000, avg_degree=24.0, gamma=2.3, seed=6)
+    g1 = P.generate(p)
+    g2 = P.generate(p)
+    check_csr(g1)
+    assert np.array_equal(g1.indptr, g2.indptr) and np.array_equal(g1.indices, g2.indices)
