@@ -466,10 +466,6 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   CUDA_TRY(cudaMemsetAsync(d_min, 0xff, 8, st));
   k_min_rp<<<4 * c->sm_count, 256, 0, st>>>(n, c->pr.as<double2>(), d_min);
   size_t tb = 0;
-  double pmin = 0.0;
-  CUDA_TRY(cudaMemcpyAsync(&pmin, d_min, 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  const double rmin = std::max(0.0, 2.0 * std::atanh(pmin) * (1.0 - 1e-12) - 1e-9);
   // window table on bands whose innermost radius is their threshold
   std::vector<Band> tbands(L);
   for (int j = 0; j < L; ++j) {
@@ -495,8 +491,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   int64_t* hi = lo + kMaxBands;
   int* mode = reinterpret_cast<int*>(hi + kMaxBands);
   float* cover = reinterpret_cast<float*>(mode + kMaxBands);
-  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows,
-                                   (int)std::floor(rmin / (double)kRowStep), sec_lo, sec_hi, lo,
+  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_min, sec_lo, sec_hi, lo,
                                    hi, mode, cover);
   c->sh_cover = cover;
   c->sh_lo = lo;

@@ -603,12 +603,17 @@ __global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, 
 // with the query radius, so rows from the smallest query radius on bound
 // every query.  Output per band, in 27-bit sort-key units: [lo, hi) of
 // needed keys (circular; lo > hi wraps), or whole = 1, or none = -1.
-__global__ void k_shard_ranges(const float* __restrict__ wtab, int L, int rows, int s0,
+__global__ void k_shard_ranges(const float* __restrict__ wtab, int L, int rows,
+                               const unsigned long long* __restrict__ pmin_bits,
                                int64_t sec_lo, int64_t sec_hi, int64_t* __restrict__ lo,
                                int64_t* __restrict__ hi, int* __restrict__ mode,
                                float* __restrict__ cover) {
   const int j = threadIdx.x;
   if (j >= L) return;
+  // row of the smallest query radius present (rounded down)
+  const double pmin = __longlong_as_double((long long)*pmin_bits);
+  const double rmin = fmax(0.0, 2.0 * atanh(pmin) * (1.0 - 1e-12) - 1e-9);
+  const int s0 = (int)floor(rmin / (double)kRowStep);
   float d = -1.0f;
   for (int s = max(s0, 0); s < rows; ++s) d = fmaxf(d, wtab[s * L + j]);
   const int64_t span = (int64_t)1 << 27;
