@@ -30,7 +30,25 @@ CONFIGS = {
     1: dict(n=1_000_000, avg_degree=10.0, gamma=3.0, seed=1),
     2: dict(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2),
     3: dict(n=100_000_000, avg_degree=16.0, gamma=3.0, seed=3),
+    4: dict(n=10_000_000, avg_degree=4.0, gamma=2.2, seed=4),  # one point; --sweep runs all 9
 }
+SWEEP = [(k, g) for k in (4.0, 64.0, 256.0) for g in (2.2, 3.0, 5.0)]
+
+
+def metric_for(params):
+    if params == CONFIGS[2]:
+        return METRIC
+    return (f"edges/sec generated (n={params['n']:.0e},k={params['avg_degree']:g},"
+            f"gamma={params['gamma']:g})").replace("e+0", "e")
+
+
+def config_params(args):
+    params = dict(CONFIGS[args.config])
+    for key, val in (("n", args.n), ("avg_degree", args.k), ("gamma", args.gamma),
+                     ("seed", args.seed)):
+        if val is not None:
+            params[key] = val
+    return params
 METRIC = "edges/sec generated (n=1e7,k=32,gamma=2.5)"
 UNIT = "edges/s"
 
@@ -54,6 +72,16 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=20_000,
                     help="query vertices per CPU-baseline step (bounded sample)")
+    ap.add_argument("--n", type=int, default=None, help="override the config's n")
+    ap.add_argument("--k", type=float, default=None, help="override the config's avg degree")
+    ap.add_argument("--gamma", type=float, default=None, help="override the config's gamma")
+    ap.add_argument("--seed", type=int, default=None, help="override the config's seed")
+    ap.add_argument("--sweep", action="store_true",
+                    help="config 4: one line per (k, gamma) point of the density/exponent "
+                         "sweep at n=1e7, seed 4 (evidence runs, not the driver's line)")
+    ap.add_argument("--shard-sim", type=int, default=0, metavar="N",
+                    help="time each of N angular shards in turn on this one GPU and report "
+                         "the per-shard times and their max (stand-in for an N-GPU run)")
     return ap.parse_args()
 
 
@@ -151,7 +179,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     import paper_1501_03545_b200 as P
-    params = CONFIGS[args.config]
+    params = config_params(args)
     gp = P.GeneratorParams(**params)
     model = gp.resolve()
     consts = P.model_constants(model.R, model.alpha)
@@ -169,7 +197,7 @@ def run_reference(args):
               f"sample all {model.n} points + build the full tree + {info['queries']} vertex "
               f"queries per step, whole-graph time extrapolated linearly in queries")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "metric": metric_for(params), "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -209,7 +237,7 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    params = CONFIGS[args.config]
+    params = config_params(args)
     gp = P.GeneratorParams(**params, vertex_order=args.vertex_order)
     model = gp.resolve()
     order = P.generator.VERTEX_ORDERS[args.vertex_order]
@@ -327,7 +355,7 @@ def run_ours(args):
             cpu = {"error": str(e)}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_for(params), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(params, model, args, world),
@@ -342,8 +370,72 @@ def run_ours(args):
     return 0
 
 
+def run_shard_sim(args):
+    """Stand-in for an N-GPU run on the one GPU a call gets: every shard of an
+    N-way angular split is generated in turn (each after its own warm-up),
+    timed with CUDA events; the N-GPU step time is the max over shards (the
+    ranks share nothing but the final edge-count all-reduce)."""
+    import torch
+
+    import paper_1501_03545_b200 as P
+    torch.cuda.set_device(0)
+    params = config_params(args)
+    gp = P.GeneratorParams(**params, vertex_order=args.vertex_order)
+    model = gp.resolve()
+    order = P.generator.VERTEX_ORDERS[args.vertex_order]
+    eng = P.get_engine(0)
+    N = args.shard_sim
+    per, nnz_all = [], 0
+    for k in range(N):
+        shard = P.Shard(k, N) if N > 1 else None
+        for _ in range(max(args.warmup, 0)):
+            eng.generate(model, params["seed"], order, shard)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        phases = {}
+        for _ in range(args.steps):
+            st = eng.generate(model, params["seed"], order, shard)
+            for key in ("t_sample_ms", "t_build_ms", "t_light_ms", "t_heavy_ms",
+                        "t_compact_ms", "t_rowsort_ms", "t_edges_ms"):
+                phases.setdefault(key, []).append(getattr(st, key))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / max(args.steps, 1)
+        nnz_all += st.nnz
+        per.append({"shard": k, "ms_per_step": ms, "nnz": st.nnz,
+                    **{key: sorted(v)[len(v) // 2] for key, v in phases.items()}})
+    ms_max = max(p["ms_per_step"] for p in per)
+    line = {"metric": metric_for(params), "unit": UNIT, "simulated_n_gpus": N,
+            "value": nnz_all / 2.0 / (ms_max / 1e3), "ms_per_step_max": ms_max,
+            "steps": args.steps, "warmup": args.warmup, "m": nnz_all / 2.0,
+            "config": config_block(params, model, args, N), "shards": per,
+            "how": "each shard run in turn on one B200 (CUDA events per shard), "
+                   "N-GPU step = max over shards"}
+    print(json.dumps(line))
+    return 0
+
+
+def run_sweep(args):
+    """BASELINE config 4: every (k, gamma) point at n=1e7, seed 4, one JSON
+    line each (evidence runs; the driver's bench line is config 2)."""
+    import subprocess as sp
+    rc = 0
+    for k, g in SWEEP:
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", "4", "--k", str(k),
+               "--gamma", str(g), "--steps", str(args.steps), "--warmup", str(args.warmup),
+               "--no-cpu-baseline", "--no-e2e", "--vertex-order", args.vertex_order]
+        rc |= sp.call(cmd)
+    return rc
+
+
 def main():
     args = parse()
+    if args.sweep:
+        return run_sweep(args)
+    if args.shard_sim:
+        return run_shard_sim(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

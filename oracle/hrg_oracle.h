@@ -64,6 +64,14 @@ int64_t orc_edges_quadtree(int64_t n, const double *phi, const double *rp, doubl
                            int64_t query_lo, int64_t query_hi,
                            int64_t cap, int64_t *u, int64_t *v, orc_qt_timing *timing);
 
+/* Full rows of the vertices qids[0..nq) by all-pairs tests: row k holds every
+ * w != qids[k] with pred(min -> max) (generator.py:182-187, quadtree.py:611-613),
+ * ascending.  For full-size parity checks of sampled rows.  Returns the total
+ * entry count; fills indptr (nq+1) and indices (up to cap) when non-NULL. */
+int64_t orc_rows_brute(int64_t n, const double *phi, const double *rp, double a, int trig,
+                       int nthreads, int64_t nq, const int64_t *qids, int64_t cap,
+                       int64_t *indptr, int64_t *indices);
+
 /* hrgen graph.py:52-77 Graph.from_edge_arrays for u<v pairs: symmetric CSR,
  * rows sorted.  indptr has n+1 entries, indices 2m. */
 void orc_csr_from_pairs(int64_t n, int64_t m, const int64_t *u, const int64_t *v,

@@ -57,6 +57,10 @@ def lib():
                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p,
                                          _i64p, ctypes.POINTER(QtTiming)]
         L.orc_edges_quadtree.restype = ctypes.c_int64
+        L.orc_rows_brute.argtypes = [ctypes.c_int64, _d, _d, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int64, _i64p, ctypes.c_int64, _i64p,
+                                     _i64p]
+        L.orc_rows_brute.restype = ctypes.c_int64
         L.orc_csr_from_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i64p, _i64p, _i64p]
         _lib = L
     return _lib
@@ -153,6 +157,24 @@ def edges_quadtree(phi, rp, a, alpha, max_r, capacity=512, trig=TRIG_LIBM, nthre
         if m <= cap:
             return np.column_stack((u[:m], v[:m])), m, tm
         cap = m
+
+
+def rows_brute(phi, rp, a, qids, trig=TRIG_LIBM, nthreads=0):
+    """Full rows (ascending neighbour ids) of the vertices qids, by all-pairs
+    tests against every point (hrgen generator.py:182-187 edge rule with the
+    quadtree.py:611-613 predicate, circle of the smaller id).  For sampled-row
+    parity at sizes where the whole edge set is out of the oracle's reach.
+    Returns (indptr (len(qids)+1,), indices) int64."""
+    phi, rp = _f64(phi), _f64(rp)
+    q = np.ascontiguousarray(qids, dtype=np.int64)
+    n = phi.size
+    total = lib().orc_rows_brute(n, _p(phi), _p(rp), a, trig, nthreads, q.size, _p(q, _i64p),
+                                 0, None, None)
+    indptr = np.empty(q.size + 1, np.int64)
+    indices = np.empty(total, np.int64)
+    lib().orc_rows_brute(n, _p(phi), _p(rp), a, trig, nthreads, q.size, _p(q, _i64p), total,
+                         _p(indptr, _i64p), _p(indices, _i64p))
+    return indptr, indices
 
 
 def csr_from_pairs(n, pairs):

@@ -54,6 +54,22 @@ def test_config0_full_edges(oracle):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("trig", [0, 1])
+def test_rows_brute_matches_whole_edge_set(oracle, trig):
+    """orc_rows_brute (sampled full rows, the full-size parity checker) equals
+    the rows of the all-pairs edge set, on reference runs incl. large R."""
+    rng = np.random.default_rng(3)
+    runs = [r for r in RUNS if r.n >= 10_000][:4] + [max(RUNS, key=lambda r: r.R)]
+    for run in runs:
+        pairs = oracle.edges_brute(run.phi, run.r_poincare, run.a, trig)
+        ip, ix = oracle.csr_from_pairs(run.n, pairs)
+        q = np.concatenate([rng.choice(run.n, 60, replace=False),
+                            np.argsort(np.diff(ip))[-4:], [0, run.n - 1]])
+        rp, ri = oracle.rows_brute(run.phi, run.r_poincare, run.a, q, trig)
+        for k, v in enumerate(q):
+            assert np.array_equal(ri[rp[k]:rp[k + 1]], ix[ip[v]:ip[v + 1]]), (run.tag, v)
+
+
 def test_trig_modes_agree_on_reference_runs(oracle):
     """Correctly rounded sin/cos (what the GPU computes) and libm (what numpy
     computes) give the same edge sets on every golden run."""
