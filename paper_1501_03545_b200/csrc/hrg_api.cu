@@ -85,7 +85,8 @@ struct hrg_context {
   Buf bands, dir, dir_total, bad, dir_gaps;
   // CSR
   Buf deg, rowptr, idx, idx2, cand;
-  Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep;
+  Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep, sh_gid;
+  bool sh_sampled = false;  // sharded sampling: vals are compact indices, sh_gid the ids
   Buf widen;
   int64_t n = 0, np = 0, nnz = 0;
   const float* sh_cover = nullptr;  // sharded subset: per-band circle coverage,
@@ -99,7 +100,7 @@ struct hrg_context {
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
-  int grid_light = 0, grid_heavy = 0, grid_compact = 0;
+  int grid_light = 0, grid_light_wide = 0, grid_heavy = 0, grid_compact = 0;
 };
 
 namespace {
@@ -152,7 +153,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   return HRG_OK;
 }
 
-inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
 double ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -182,12 +183,12 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
     k_gather<true><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
         c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
-        nullptr);
+        nullptr, c->sh_sampled ? c->sh_gid.as<int32_t>() : nullptr, c->vals_out.as<int32_t>());
   else
     k_gather<false><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
         c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
-        c->s_rn.as<double>());
+        c->s_rn.as<double>(), nullptr, nullptr);
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     // sector bounds on the sort granularity (multiples of 2^kSortShift)
@@ -297,7 +298,17 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   }
 
   if (c->grid_light == 0) {
-    c->grid_light = occupancy_grid(c, k_light<true>, kLightThreads);
+    for (auto kern : {k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>,
+                      k_light<false, kSegCap, HRG_LIGHT_MINBLOCKS>})
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)light_smem<kSegCap>()));
+    for (auto kern : {k_light<true, kSegCapWide, 4>, k_light<false, kSegCapWide, 4>})
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)light_smem<kSegCapWide>()));
+    c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads,
+                                   light_smem<kSegCap>());
+    c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, 4>, kLightThreads,
+                                        light_smem<kSegCapWide>());
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     // (k_compact_heavy shares the heavy grid: both walk the chunk list)
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
@@ -310,8 +321,23 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sort_rows_smem<kLargeMax, 2>()));
   }
+  // segment slots per light query: the wide variant when most of the 32
+  // bands hold points (expected >= 1 point per band, from the radial CDF
+  // (cosh(alpha r) - 1) / (cosh(alpha R) - 1)), so light queries reach them all
+  bool wide = false;
+  {
+    int populated = 0;
+    const double den = std::cosh(M->alpha * M->R) - 1.0;
+    for (int j = 0; j < L; ++j) {
+      const double f0 = (std::cosh(M->alpha * M->R * j / L) - 1.0) / den;
+      const double f1 = (std::cosh(M->alpha * M->R * (j + 1) / L) - 1.0) / den;
+      populated += (double)n * (f1 - f0) >= 1.0;
+    }
+    wide = populated >= kWideBands;
+    if (const char* e = getenv("HRG_LIGHT_WIDE")) wide = atoi(e) != 0;
+  }
   unsigned gq = (unsigned)std::max<int64_t>(
-      1, std::min<int64_t>(blocks_for(np, kLightThreads), c->grid_light));
+      1, std::min<int64_t>(blocks_for(np, kLightThreads), wide ? c->grid_light_wide : c->grid_light));
   unsigned gc = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
@@ -345,8 +371,14 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
-    if (sample_ids) k_light<true><<<gq, kLightThreads, 0, st>>>(A);
-    else k_light<false><<<gq, kLightThreads, 0, st>>>(A);
+    {
+      constexpr int MB = HRG_LIGHT_MINBLOCKS;
+      const size_t sn = light_smem<kSegCap>(), sw = light_smem<kSegCapWide>();
+      if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, sn, st>>>(A);
+      else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, sn, st>>>(A);
+      else if (sample_ids) k_light<true, kSegCapWide, 4><<<gq, kLightThreads, sw, st>>>(A);
+      else k_light<false, kSegCapWide, 4><<<gq, kLightThreads, sw, st>>>(A);
+    }
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
     k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),
                                      c->chunk_start.as<int64_t>(), c->chunk_entry.as<int32_t>(),
@@ -529,6 +561,70 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   return HRG_OK;
 }
 
+// Sharded runs sampling their own points (sample ids): the sector's
+// smallest radius, the reachable range of every band, then one sampling
+// pass that keeps (and evaluates the radius of) only the reachable points
+// (DESIGN.md "Multi-GPU").  Replaces k_sample + shard_subset.
+hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_shard* shard,
+                        const SampleParams& P) {
+  const int64_t n = M->n;
+  cudaStream_t st = c->stream;
+  ShardSample S;
+  memset(&S, 0, sizeof(S));
+  S.L = L;
+  // band thresholds on the radial uniform: the inverse CDF at r_j = R j / L
+  // (any increasing sequence is correct; this one matches the radial bands)
+  const double two53 = std::ldexp(1.0, 53);
+  for (int j = 1; j < L; ++j) {
+    const double rj = M->R * j / L;
+    const double u = std::pow(std::sinh(M->alpha * rj / 2.0) / M->sinh_half_alpha_r, 2.0);
+    double b = std::ceil(u * two53);
+    if (!(b < two53)) b = two53;
+    S.ub[j] = std::max<uint64_t>((uint64_t)b, S.ub[j - 1] + 1);
+  }
+  const int64_t span = (int64_t)1 << 27;
+  S.sec_lo = ((int64_t)shard->index * span + shard->count - 1) / shard->count;
+  S.sec_hi = shard->index + 1 == shard->count
+                 ? span
+                 : ((int64_t)(shard->index + 1) * span + shard->count - 1) / shard->count;
+  CUDA_TRY(c->sh_buf.ensure(1024));
+  unsigned long long* d_umin = reinterpret_cast<unsigned long long*>(c->sh_buf.p);
+  unsigned long long* d_pmin = d_umin + 1;
+  unsigned* d_cnt = reinterpret_cast<unsigned*>(c->sh_buf.as<char>() + 960);
+  CUDA_TRY(cudaMemsetAsync(d_umin, 0xff, 8, st));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
+  k_shard_umin<<<8 * c->sm_count, 256, 0, st>>>(n, P, S, d_umin);
+  const int rows = (int)std::ceil(M->R / (double)kRowStep) + 2;
+  CUDA_TRY(c->sh_bands.ensure(sizeof(Band) * L));
+  CUDA_TRY(c->sh_wtab.ensure(sizeof(float) * (size_t)rows * L));
+  k_shard_prep<<<1, 32, 0, st>>>(P, S, d_umin, c->sh_bands.as<Band>(), d_pmin);
+  k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
+                                      std::ldexp(1.0, -45), c->sh_wtab.as<float>());
+  int64_t* lo = reinterpret_cast<int64_t*>(c->sh_buf.as<char>() + 64);
+  int64_t* hi = lo + kMaxBands;
+  int* mode = reinterpret_cast<int*>(hi + kMaxBands);
+  float* cover = reinterpret_cast<float*>(mode + kMaxBands);
+  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_pmin, S.sec_lo, S.sec_hi,
+                                   lo, hi, mode, cover);
+  c->sh_cover = cover;
+  c->sh_lo = lo;
+  c->sh_hi = hi;
+  c->sh_mode = mode;
+  CUDA_TRY(c->dir.ensure(4 * (size_t)((4 * n << kDirExtra) + 2 * kMaxBands + 64)));
+  CUDA_TRY(c->sh_gid.ensure(4 * (size_t)n));
+  k_shard_sample<<<blocks_for(n, 256 * kShardPer), 256, 0, st>>>(n, P, S, lo, hi, mode, c->k32_in.as<uint32_t>(),
+                                                c->vals_in.as<int32_t>(), c->pr.as<double2>(),
+                                                c->sh_gid.as<int32_t>(), d_cnt);
+  k_shard_radius<<<8 * c->sm_count, 256, 0, st>>>(P, d_cnt, c->pr.as<double2>());
+  CUDA_TRY(cudaGetLastError());
+  unsigned np = 0;
+  CUDA_TRY(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  c->np = np;
+  c->sh_sampled = true;
+  return HRG_OK;
+}
+
 hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* shard,
                         bool sample_ids, bool from_coords, uint64_t seed, hrg_stats* stats) {
   int64_t n = M->n;
@@ -544,7 +640,15 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     stats->n_bands = L;
   }
   CUDA_TRY(cudaEventRecord(c->ev[E_START], st));
-  if (!from_coords) {
+  c->sh_sampled = false;
+  const bool shard_sampling = !from_coords && shard && shard->count > 1 && sample_ids;
+  if (shard_sampling) {
+    SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
+    hrg_status s0 = shard_sample(c, M, L, shard, P);
+    if (s0 != HRG_OK) return s0;
+    c->coords_pending = true;
+    c->pending = P;
+  } else if (!from_coords) {
     SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
     // coordinates on request only (hrg_result_device_ptrs); angular order
     // gathers r_native into its sorted copy, so that one is written
@@ -568,9 +672,9 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   }
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(c->ev[E_SAMPLED], st));
-  c->np = n;
+  if (!shard_sampling) c->np = n;
   hrg_status s = HRG_OK;
-  if (shard && shard->count > 1 && sample_ids) {
+  if (!shard_sampling && shard && shard->count > 1 && sample_ids) {
     s = shard_subset(c, M, S, L, shard);
     if (s != HRG_OK) return s;
   }
@@ -630,7 +734,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps,
-                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep,
+                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})
     b->release();
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);

@@ -128,17 +128,31 @@ __device__ __forceinline__ uint32_t sort_key32(int band, uint64_t q) {
 // hrgen generator.py:160-179 with a counter-based stream: vertex i draws its
 // angle from the first and its radius from the second 53-bit uniform of
 // Philox4x32-10(counter = i, key = seed).
-__device__ __forceinline__ void sample_point(int64_t i, const SampleParams& P, double& ph,
-                                             double& r, double& p) {
+__device__ __forceinline__ void philox_u53(int64_t i, uint64_t seed, uint64_t& a, uint64_t& b) {
   uint32_t c[4] = {(uint32_t)i, (uint32_t)((uint64_t)i >> 32), 0u, 0u};
-  philox4x32_10(c, (uint32_t)P.seed, (uint32_t)(P.seed >> 32));
-  uint64_t a = (((uint64_t)c[1] << 32) | c[0]) >> 11;
-  uint64_t b = (((uint64_t)c[3] << 32) | c[2]) >> 11;
-  double u1 = (double)a * 0x1.0p-53, u2 = (double)b * 0x1.0p-53;
-  ph = __dmul_rn(kTwoPi, u1);                                          // :170
+  philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  a = (((uint64_t)c[1] << 32) | c[0]) >> 11;
+  b = (((uint64_t)c[3] << 32) | c[2]) >> 11;
+}
+
+__device__ __forceinline__ double angle_from_u53(uint64_t a) {
+  return __dmul_rn(kTwoPi, (double)a * 0x1.0p-53);                    // :170
+}
+
+__device__ __forceinline__ void radius_from_u53(uint64_t b, const SampleParams& P, double& r,
+                                                double& p) {
+  const double u2 = (double)b * 0x1.0p-53;
   r = __dmul_rn(P.two_over_alpha, asinh(__dmul_rn(__dsqrt_rn(u2), P.sinh_half)));
   r = fmin(r, P.r_cap);                                                // :174
   p = fmin(tanh(__dmul_rn(r, 0.5)), P.rp_cap);                        // :175-178
+}
+
+__device__ __forceinline__ void sample_point(int64_t i, const SampleParams& P, double& ph,
+                                             double& r, double& p) {
+  uint64_t a, b;
+  philox_u53(i, P.seed, a, b);
+  ph = angle_from_u53(a);
+  radius_from_u53(b, P, r, p);
 }
 
 // The pipeline's sampler: packed (phi, r_p), sort key and id per vertex; the
@@ -241,17 +255,23 @@ struct QRec {          // query-side extras, per sorted position
 // granularity, instead of one per array); the full key is rebuilt from the
 // band bits of the sort key and qkey(phi), the same function k_sample used.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __restrict__ perm,
+__global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
                                                 const uint32_t* __restrict__ k32,
                                                 uint64_t* __restrict__ keys_out, double C,
                                                 const double2* __restrict__ pr,
                                                 const double* __restrict__ rn, double a,
                                                 Recs rec, QRec q,
                                                 double* __restrict__ s_rp,
-                                                double* __restrict__ s_rn) {
+                                                double* __restrict__ s_rn,
+                                                const int32_t* __restrict__ gid,
+                                                int32_t* ids_out) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
-  int32_t i = perm[p];
+  const int32_t i = perm[p];
+  // sharded sampling: perm holds compact indices; ids_out (== perm) gets
+  // the global vertex id in place (same element, same thread)
+  const int32_t id = gid ? __ldg(gid + i) : i;
+  if (gid) ids_out[p] = id;
   const double2 q2 = pr[i];
   const double ph = q2.x, r = q2.y;
   keys_out[p] = ((uint64_t)(k32[p] >> 27) << kQBits) | qkey(ph, C);
@@ -263,7 +283,7 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* __rest
   const double cx = __dmul_rn(cr, cs), cy = __dmul_rn(cr, sn), rsq = __dmul_rn(rad, rad);
   if (kSampleIds) {
     Rec R;
-    R.px = px; R.py = py; R.cx = cx; R.cy = cy; R.rsq = rsq; R.id = i; R.pad = 0;
+    R.px = px; R.py = py; R.cx = cx; R.cy = cy; R.rsq = rsq; R.id = id; R.pad = 0;
     rec.rec[p] = R;
   } else {
     rec.pt[p] = make_double2(px, py);
@@ -628,18 +648,177 @@ __global__ void k_shard_ranges(const float* __restrict__ wtab, int L, int rows,
   cover[j] = (float)((double)(2 * dk + (sec_hi - sec_lo)) / (double)span);
 }
 
+// Does band b's reachable range (k_shard_ranges) hold 27-bit angle q?
+__device__ __forceinline__ bool shard_keep(int b, int64_t q, const int64_t* lo,
+                                           const int64_t* hi, const int* mode) {
+  const int md = mode[b];
+  bool ok = md > 0;
+  if (md == 0) ok = lo[b] <= hi[b] ? (q >= lo[b] && q < hi[b]) : (q >= lo[b] || q < hi[b]);
+  return ok;
+}
+
 __global__ void k_shard_flags(int64_t n, const uint32_t* __restrict__ k32,
                               const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
                               const int* __restrict__ mode, uint8_t* __restrict__ keep) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t k = k32[i];
-  const int b = (int)(k >> 27);
-  const int64_t q = (int64_t)(k & ((1u << 27) - 1));
-  const int md = mode[b];
-  bool ok = md > 0;
-  if (md == 0) ok = lo[b] <= hi[b] ? (q >= lo[b] && q < hi[b]) : (q >= lo[b] || q < hi[b]);
-  keep[i] = ok ? 1 : 0;
+  keep[i] = shard_keep((int)(k >> 27), (int64_t)(k & ((1u << 27) - 1)), lo, hi, mode) ? 1 : 0;
+}
+
+// ---- sharded sampling (sample ids).  A rank needs only the points its
+// sector's queries can reach, and those are decided by the angle and the
+// band alone, so the radius (asinh + tanh, the sampler's FP64 cost) is
+// evaluated for the kept points only.  Bands are cut on the radial uniform:
+// band(b) = #{ j in [1, L) : b >= ub[j] } on the 53-bit integer b behind u2,
+// any increasing ub works; k_shard_prep bounds each band's innermost radius
+// from below by evaluating the sampler at ub[j].
+struct ShardSample {
+  uint64_t ub[kMaxBands];  // band thresholds on the 53-bit radial uniform
+  int L;
+  int64_t sec_lo, sec_hi;  // this rank's sector, 27-bit angle units
+};
+
+// Smallest radial uniform among the sector's vertices (its queries' widest
+// windows come from the smallest radius, which is monotone in it).
+__global__ void __launch_bounds__(256) k_shard_umin(int64_t n, SampleParams P, ShardSample S,
+                                                    unsigned long long* __restrict__ out) {
+  unsigned long long m = ~0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t a, b;
+    philox_u53(i, P.seed, a, b);
+    const int64_t q = (int64_t)(qkey(angle_from_u53(a), P.C) >> kSortShift);
+    if (q >= S.sec_lo && q < S.sec_hi) m = min(m, (unsigned long long)b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(out, m);
+}
+
+// Lower bounds of each band's innermost Poincare radius (the sampler at the
+// band's threshold, 16 ulps down: asinh/tanh are monotone to a few ulps) as
+// window-table bands, and the smallest query radius of the sector (0 when
+// the sector is empty: the widest windows, always safe).
+__global__ void k_shard_prep(SampleParams P, ShardSample S,
+                             const unsigned long long* __restrict__ umin, Band* __restrict__ tb,
+                             unsigned long long* __restrict__ pmin_bits) {
+  const int j = threadIdx.x;
+  if (j < S.L) {
+    double r, p = 0.0;
+    if (j > 0) {
+      radius_from_u53(S.ub[j], P, r, p);
+      for (int k = 0; k < 16; ++k) p = nextafter(p, 0.0);
+    }
+    Band B;
+    memset(&B, 0, sizeof(B));
+    B.start = 0; B.end = 1; B.pmin = p;
+    tb[j] = B;
+  }
+  if (j == 0) {
+    double r, p = 0.0;
+    if (*umin != ~0ull) radius_from_u53(*umin, P, r, p);
+    *pmin_bits = (unsigned long long)__double_as_longlong(p);
+  }
+}
+
+// The kept points' sort keys, compact indices (the sort's values), packed
+// (phi, r_p) and global ids.  A block takes kShardPer points per thread and
+// reserves its output with one atomic (one per warp serialises on the
+// counter).  The order of kept points is arbitrary: ties of the 32-bit sort
+// key may land in any order, which changes no row (rows are sorted by id)
+// and no window (exact trims hold on any order).
+constexpr int kShardPer = 8;
+__global__ void __launch_bounds__(256) k_shard_sample(int64_t n, SampleParams P, ShardSample S,
+                                                      const int64_t* __restrict__ lo,
+                                                      const int64_t* __restrict__ hi,
+                                                      const int* __restrict__ mode,
+                                                      uint32_t* __restrict__ keys,
+                                                      int32_t* __restrict__ vals,
+                                                      double2* __restrict__ pr,
+                                                      int32_t* __restrict__ gid,
+                                                      unsigned* __restrict__ count) {
+  __shared__ unsigned wcnt[8], wbase[8], bbase;
+  __shared__ uint64_t s_ub[kMaxBands];
+  __shared__ int64_t s_lo[kMaxBands], s_hi[kMaxBands];
+  __shared__ int s_mode[kMaxBands];
+  if (threadIdx.x < kMaxBands) {
+    const int j = threadIdx.x;
+    s_ub[j] = j < S.L ? S.ub[j] : ~0ull;
+    s_lo[j] = j < S.L ? lo[j] : 0;
+    s_hi[j] = j < S.L ? hi[j] : 0;
+    s_mode[j] = j < S.L ? mode[j] : -1;
+  }
+  __syncthreads();
+  // band = #{ j in [1, L) : b >= ub[j] } by binary search (ub increasing)
+  auto band_of = [&](uint64_t b) {
+    int k = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1)
+      if (b >= s_ub[k + st]) k += st;
+    return k;
+  };
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * (256 * kShardPer) + threadIdx.x;
+  uint64_t ua[kShardPer], ub[kShardPer];
+  unsigned kmask = 0;
+#pragma unroll
+  for (int k = 0; k < kShardPer; ++k) {
+    const int64_t i = i0 + 256 * k;
+    ua[k] = ub[k] = 0;
+    if (i < n) {
+      philox_u53(i, P.seed, ua[k], ub[k]);
+      const uint64_t q = qkey(angle_from_u53(ua[k]), P.C);
+      if (shard_keep(band_of(ub[k]), (int64_t)(q >> kSortShift), s_lo, s_hi, s_mode))
+        kmask |= 1u << k;
+    }
+  }
+  // rank of each kept point: k-major, then warp, then lane
+  unsigned warp_tot = 0;
+  unsigned ballots[kShardPer];
+#pragma unroll
+  for (int k = 0; k < kShardPer; ++k) {
+    ballots[k] = __ballot_sync(0xffffffffu, (kmask >> k) & 1u);
+    warp_tot += __popc(ballots[k]);
+  }
+  if (lane == 0) wcnt[w] = warp_tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int k = 0; k < 8; ++k) { wbase[k] = t; t += wcnt[k]; }
+    bbase = t ? atomicAdd(count, t) : 0u;
+  }
+  __syncthreads();
+  unsigned pos = bbase + wbase[w];
+#pragma unroll
+  for (int k = 0; k < kShardPer; ++k) {
+    if ((kmask >> k) & 1u) {
+      const unsigned at = pos + __popc(ballots[k] & ((1u << lane) - 1u));
+      const double ph = angle_from_u53(ua[k]);
+      keys[at] = sort_key32(band_of(ub[k]), qkey(ph, P.C));
+      vals[at] = (int32_t)at;
+      // the radius is evaluated densely by k_shard_radius: here only a few
+      // lanes of a warp keep their point, and a divergent asinh + tanh costs
+      // the whole warp
+      pr[at] = make_double2(ph, __longlong_as_double((long long)ub[k]));
+      gid[at] = (int32_t)(i0 + 256 * k);
+    }
+    pos += __popc(ballots[k]);
+  }
+}
+
+// Radii of the kept points (dense over the compacted range): pr[i].y holds
+// the radial uniform's 53-bit integer on entry, r_p on exit.
+__global__ void __launch_bounds__(256) k_shard_radius(SampleParams P,
+                                                      const unsigned* __restrict__ count,
+                                                      double2* __restrict__ pr) {
+  const int64_t m = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double r, p;
+    radius_from_u53((uint64_t)__double_as_longlong(pr[i].y), P, r, p);
+    pr[i].y = p;
+  }
 }
 
 // Window of band B for a query at angle phi with table half-width dlt, as
@@ -861,24 +1040,40 @@ __device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, i
 }
 
 constexpr int kWalkUnroll = HRG_WALK_UNROLL;  // walk steps whose loads are in flight together
-constexpr int kSegStride = kSegCap + 1;
 constexpr int kFirstSeg = 1 << 30;            // flat entry: the query's first segment
-constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | lane  // per-lane segment slots, padded against bank conflicts
+constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | lane
 
+// Per-lane segment slots (kCap + 1 stride, padded against bank conflicts).
+// Two variants: kSegCap slots at 6 blocks/SM, and kSegCapWide slots at 4
+// blocks/SM for models whose queries reach most of the 32 bands (small
+// alpha: every band populated, so a light query holds up to 32 segments plus
+// wrap-around splits; with the narrow variant nearly all of them would be
+// deferred to the per-query heavy path).
+constexpr int kSegCapWide = 40;
+constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
+template <int kCap>
 struct LightSmem {
-  int2 flat[kLightThreads / 32][32 * kSegStride];  // per warp: the tile's band segments
+  static constexpr int kStride = kCap + 1;
+  int2 flat[kLightThreads / 32][32 * kStride];  // per warp: the tile's band segments
   QFull q[kLightThreads];
   int32_t hits[kLightThreads];
 };
 
-__device__ __forceinline__ const QFull& f_of(const LightSmem& sm, int q) { return sm.q[q]; }
+template <int kCap>
+__device__ __forceinline__ const QFull& f_of(const LightSmem<kCap>& sm, int q) { return sm.q[q]; }
 
-// Queries with more than kLightMax candidates or kSegCap segments are
-// deferred to k_heavy.
-template <bool kSampleIds>
-__global__ void __launch_bounds__(kLightThreads, HRG_LIGHT_MINBLOCKS) k_light(QueryArgs A) {
+template <int kCap>
+constexpr size_t light_smem() { return sizeof(LightSmem<kCap>); }
+
+// Queries with more than kLightMax candidates or kCap segments are deferred
+// to k_heavy.
+template <bool kSampleIds, int kCap, int kMinBlocks>
+__global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A) {
+  constexpr int kSegCap = kCap;
+  constexpr int kSegStride = LightSmem<kCap>::kStride;
   __shared__ Band sb[kMaxBands];
-  __shared__ LightSmem sm;
+  extern __shared__ __align__(16) unsigned char light_dyn[];
+  LightSmem<kCap>& sm = *reinterpret_cast<LightSmem<kCap>*>(light_dyn);
   load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;

@@ -207,6 +207,31 @@ def test_shards_partition_the_rows():
             assert np.array_equal(g.neighbors(v), full.neighbors(v))
 
 
+@pytest.mark.parametrize("kw,count", [
+    (dict(n=5, radius=3.0, alpha=1.0, seed=1), 8),
+    (dict(n=3_000, avg_degree=8.0, gamma=3.0, seed=2), 7),
+    (dict(n=100_000, radius=35.50799080982715, alpha=0.6, seed=4), 8),
+    (dict(n=300_000, avg_degree=64.0, gamma=2.2, seed=4), 8),
+], ids=["n5-x8", "n3000-x7", "R35.5-x8", "k64-g2.2-x8"])
+def test_shards_union_is_the_graph(kw, count):
+    """Sharded sampling (each rank samples and indexes only the points its
+    sector can reach) reproduces the single-GPU graph row for row."""
+    p = GeneratorParams(**kw)
+    full = P.generate(p)
+    acc = np.zeros(full.n, np.int64)
+    for k in range(count):
+        g, _ = P.generate_with_stats(p, shard=P.Shard(k, count))
+        deg = np.diff(g.indptr)
+        assert np.all(acc[deg > 0] == 0)
+        acc += deg
+        rows = np.flatnonzero(deg)
+        if rows.size:
+            sel = np.concatenate([rows[:300], rows[np.argsort(deg[rows])[-20:]]])
+            for v in sel:
+                assert np.array_equal(g.neighbors(v), full.neighbors(v))
+    assert np.array_equal(acc, np.diff(full.indptr))
+
+
 # ------------------------------------------------------------ properties
 def test_full_size_config2_properties():
     """BASELINE config 2 (n=1e7, k=32, gamma=2.5, seed 2): hrgen Graph
