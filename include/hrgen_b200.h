@@ -146,6 +146,13 @@ hrg_status hrg_host_free(void *p);
  * p_x = r*cos(phi), quadtree.py:474) for n host angles in [0, 2pi). */
 hrg_status hrg_debug_sincos(hrg_context *ctx, int64_t n, const double *x, double *s, double *c);
 
+/* Diagnostic: the sampler-side fast sin/cos (table + short series + rounding
+ * test) against the full double-double evaluation on n seeded angles (every
+ * 4th within 2^-20 of a multiple of pi/4): values that differ, and values
+ * the fast path's rounding test sent to the full evaluation. */
+hrg_status hrg_debug_sincos_compare(hrg_context *ctx, int64_t n, uint64_t seed,
+                                    int64_t *mismatches, int64_t *rejected);
+
 /* Wait for all work queued by ctx. */
 hrg_status hrg_synchronize(hrg_context *ctx);
 

@@ -593,7 +593,7 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
   unsigned* d_cnt = reinterpret_cast<unsigned*>(c->sh_buf.as<char>() + 960);
   CUDA_TRY(cudaMemsetAsync(d_umin, 0xff, 8, st));
   CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
-  k_shard_umin<<<8 * c->sm_count, 256, 0, st>>>(n, P, S, d_umin);
+  k_shard_keys<<<8 * c->sm_count, 256, 0, st>>>(n, P, S, c->k32_out.as<uint32_t>(), d_umin);
   const int rows = (int)std::ceil(M->R / (double)kRowStep) + 2;
   CUDA_TRY(c->sh_bands.ensure(sizeof(Band) * L));
   CUDA_TRY(c->sh_wtab.ensure(sizeof(float) * (size_t)rows * L));
@@ -612,10 +612,11 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
   c->sh_mode = mode;
   CUDA_TRY(c->dir.ensure(4 * (size_t)((4 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->sh_gid.ensure(4 * (size_t)n));
-  k_shard_sample<<<blocks_for(n, 256 * kShardPer), 256, 0, st>>>(n, P, S, lo, hi, mode, c->k32_in.as<uint32_t>(),
-                                                c->vals_in.as<int32_t>(), c->pr.as<double2>(),
-                                                c->sh_gid.as<int32_t>(), d_cnt);
-  k_shard_radius<<<8 * c->sm_count, 256, 0, st>>>(P, d_cnt, c->pr.as<double2>());
+  k_shard_select<<<blocks_for(n, 256 * kShardPer), 256, 0, st>>>(
+      n, L, c->k32_out.as<uint32_t>(), lo, hi, mode, c->k32_in.as<uint32_t>(),
+      c->vals_in.as<int32_t>(), c->sh_gid.as<int32_t>(), d_cnt);
+  k_shard_points<<<8 * c->sm_count, 256, 0, st>>>(P, d_cnt, c->sh_gid.as<int32_t>(),
+                                                  c->pr.as<double2>());
   CUDA_TRY(cudaGetLastError());
   unsigned np = 0;
   CUDA_TRY(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
@@ -718,6 +719,11 @@ hrg_status hrg_context_create(int device, void* cuda_stream, hrg_context** out) 
     cudaError_t r = cudaEventCreate(&e);
     if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
   }
+  // the sin/cos table of the fast path (device-global, idempotent)
+  k_sincos_table<<<1, 256, 0, c->stream>>>();
+  cudaError_t r = cudaStreamSynchronize(c->stream);
+  if (r == cudaSuccess) r = cudaGetLastError();
+  if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
   *out = c;
   return HRG_OK;
 }
@@ -947,6 +953,25 @@ hrg_status hrg_host_free(void* p) {
   return HRG_OK;
 }
 
+hrg_status hrg_debug_sincos_compare(hrg_context* c, int64_t n, uint64_t seed,
+                                    int64_t* mismatches, int64_t* rejected) {
+  if (!c || n < 0 || !mismatches || !rejected)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  Buf b;
+  CUDA_TRY(b.ensure(16));
+  cudaStream_t st = c->stream;
+  CUDA_TRY(cudaMemsetAsync(b.p, 0, 16, st));
+  k_sincos_compare<<<8 * c->sm_count, 256, 0, st>>>(n, seed, b.as<unsigned long long>());
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, b.p, 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *mismatches = (int64_t)h[0];
+  *rejected = (int64_t)h[1];
+  return HRG_OK;
+}
+
 hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, double* s, double* co) {
   if (!c || n < 0 || !x || !s || !co) return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
   if (n == 0) return HRG_OK;
@@ -956,7 +981,7 @@ hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, double* 
   double* d = b.as<double>();
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemcpyAsync(d, x, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
-  k_sincos<<<blocks_for(n), 256, 0, st>>>(n, d, d + n, d + 2 * n);
+  k_sincos<<<blocks_for(n), 256, 0, st>>>(n, d, d + n, d + 2 * n, false);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(s, d + n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(co, d + 2 * n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));

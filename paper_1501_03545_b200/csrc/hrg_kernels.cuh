@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
   const double ph = q2.x, r = q2.y;
   keys_out[p] = ((uint64_t)(k32[p] >> 27) << kQBits) | qkey(ph, C);
   double sn, cs;
-  sincos_cr(ph, &sn, &cs);
+  sincos_crf(ph, &sn, &cs);
   double cr, rad;
   circle_params(r, a, &cr, &rad);
   const double px = __dmul_rn(r, cs), py = __dmul_rn(r, sn);
@@ -679,17 +679,31 @@ struct ShardSample {
   int64_t sec_lo, sec_hi;  // this rank's sector, 27-bit angle units
 };
 
-// Smallest radial uniform among the sector's vertices (its queries' widest
-// windows come from the smallest radius, which is monotone in it).
-__global__ void __launch_bounds__(256) k_shard_umin(int64_t n, SampleParams P, ShardSample S,
+// Pass 1 over all draws: every vertex's 32-bit sort key (band from the
+// radial uniform, binary search over ub[] in shared memory; angle from the
+// first uniform) and the smallest radial uniform among the sector's vertices
+// (its queries' widest windows come from the smallest radius, which is
+// monotone in it).  The keep decision then reads 4 B per draw instead of
+// evaluating Philox a second time.
+__global__ void __launch_bounds__(256) k_shard_keys(int64_t n, SampleParams P, ShardSample S,
+                                                    uint32_t* __restrict__ keys,
                                                     unsigned long long* __restrict__ out) {
+  __shared__ uint64_t s_ub[kMaxBands];
+  if (threadIdx.x < kMaxBands) s_ub[threadIdx.x] = threadIdx.x < S.L ? S.ub[threadIdx.x] : ~0ull;
+  __syncthreads();
   unsigned long long m = ~0ull;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t a, b;
     philox_u53(i, P.seed, a, b);
-    const int64_t q = (int64_t)(qkey(angle_from_u53(a), P.C) >> kSortShift);
-    if (q >= S.sec_lo && q < S.sec_hi) m = min(m, (unsigned long long)b);
+    const uint64_t q = qkey(angle_from_u53(a), P.C);
+    int band = 0;
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1)
+      if (b >= s_ub[band + st]) band += st;
+    keys[i] = sort_key32(band, q);
+    const int64_t q27 = (int64_t)(q >> kSortShift);
+    if (q27 >= S.sec_lo && q27 < S.sec_hi) m = min(m, (unsigned long long)b);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -722,63 +736,44 @@ __global__ void k_shard_prep(SampleParams P, ShardSample S,
   }
 }
 
-// The kept points' sort keys, compact indices (the sort's values), packed
-// (phi, r_p) and global ids.  A block takes kShardPer points per thread and
-// reserves its output with one atomic (one per warp serialises on the
-// counter).  The order of kept points is arbitrary: ties of the 32-bit sort
-// key may land in any order, which changes no row (rows are sorted by id)
-// and no window (exact trims hold on any order).
+// Pass 2: the kept draws' sort keys, compact indices (the sort's values)
+// and global ids.  A block takes kShardPer draws per thread and reserves its
+// output with one atomic (one per warp serialises on the counter).  The
+// order of kept points is arbitrary: ties of the 32-bit sort key may land in
+// any order, which changes no row (rows are sorted by id) and no window
+// (exact trims hold on any order).
 constexpr int kShardPer = 8;
-__global__ void __launch_bounds__(256) k_shard_sample(int64_t n, SampleParams P, ShardSample S,
+__global__ void __launch_bounds__(256) k_shard_select(int64_t n, int L,
+                                                      const uint32_t* __restrict__ keys_all,
                                                       const int64_t* __restrict__ lo,
                                                       const int64_t* __restrict__ hi,
                                                       const int* __restrict__ mode,
                                                       uint32_t* __restrict__ keys,
                                                       int32_t* __restrict__ vals,
-                                                      double2* __restrict__ pr,
                                                       int32_t* __restrict__ gid,
                                                       unsigned* __restrict__ count) {
   __shared__ unsigned wcnt[8], wbase[8], bbase;
-  __shared__ uint64_t s_ub[kMaxBands];
   __shared__ int64_t s_lo[kMaxBands], s_hi[kMaxBands];
   __shared__ int s_mode[kMaxBands];
   if (threadIdx.x < kMaxBands) {
     const int j = threadIdx.x;
-    s_ub[j] = j < S.L ? S.ub[j] : ~0ull;
-    s_lo[j] = j < S.L ? lo[j] : 0;
-    s_hi[j] = j < S.L ? hi[j] : 0;
-    s_mode[j] = j < S.L ? mode[j] : -1;
+    s_lo[j] = j < L ? lo[j] : 0;
+    s_hi[j] = j < L ? hi[j] : 0;
+    s_mode[j] = j < L ? mode[j] : -1;
   }
   __syncthreads();
-  // band = #{ j in [1, L) : b >= ub[j] } by binary search (ub increasing)
-  auto band_of = [&](uint64_t b) {
-    int k = 0;
-#pragma unroll
-    for (int st = 16; st > 0; st >>= 1)
-      if (b >= s_ub[k + st]) k += st;
-    return k;
-  };
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i0 = (int64_t)blockIdx.x * (256 * kShardPer) + threadIdx.x;
-  uint64_t ua[kShardPer], ub[kShardPer];
-  unsigned kmask = 0;
+  uint32_t kk[kShardPer];
+  unsigned ballots[kShardPer];
+  unsigned warp_tot = 0;
 #pragma unroll
   for (int k = 0; k < kShardPer; ++k) {
     const int64_t i = i0 + 256 * k;
-    ua[k] = ub[k] = 0;
-    if (i < n) {
-      philox_u53(i, P.seed, ua[k], ub[k]);
-      const uint64_t q = qkey(angle_from_u53(ua[k]), P.C);
-      if (shard_keep(band_of(ub[k]), (int64_t)(q >> kSortShift), s_lo, s_hi, s_mode))
-        kmask |= 1u << k;
-    }
-  }
-  // rank of each kept point: k-major, then warp, then lane
-  unsigned warp_tot = 0;
-  unsigned ballots[kShardPer];
-#pragma unroll
-  for (int k = 0; k < kShardPer; ++k) {
-    ballots[k] = __ballot_sync(0xffffffffu, (kmask >> k) & 1u);
+    kk[k] = i < n ? __ldg(keys_all + i) : 0u;
+    const bool keep = i < n && shard_keep((int)(kk[k] >> 27), (int64_t)(kk[k] & ((1u << 27) - 1)),
+                                          s_lo, s_hi, s_mode);
+    ballots[k] = __ballot_sync(0xffffffffu, keep);
     warp_tot += __popc(ballots[k]);
   }
   if (lane == 0) wcnt[w] = warp_tot;
@@ -792,32 +787,28 @@ __global__ void __launch_bounds__(256) k_shard_sample(int64_t n, SampleParams P,
   unsigned pos = bbase + wbase[w];
 #pragma unroll
   for (int k = 0; k < kShardPer; ++k) {
-    if ((kmask >> k) & 1u) {
+    if ((ballots[k] >> lane) & 1u) {
       const unsigned at = pos + __popc(ballots[k] & ((1u << lane) - 1u));
-      const double ph = angle_from_u53(ua[k]);
-      keys[at] = sort_key32(band_of(ub[k]), qkey(ph, P.C));
+      keys[at] = kk[k];
       vals[at] = (int32_t)at;
-      // the radius is evaluated densely by k_shard_radius: here only a few
-      // lanes of a warp keep their point, and a divergent asinh + tanh costs
-      // the whole warp
-      pr[at] = make_double2(ph, __longlong_as_double((long long)ub[k]));
       gid[at] = (int32_t)(i0 + 256 * k);
     }
     pos += __popc(ballots[k]);
   }
 }
 
-// Radii of the kept points (dense over the compacted range): pr[i].y holds
-// the radial uniform's 53-bit integer on entry, r_p on exit.
-__global__ void __launch_bounds__(256) k_shard_radius(SampleParams P,
+// Pass 3, dense over the kept points: (phi, r_p) from the vertex's own draws
+// (Philox again for a quarter of the draws; asinh + tanh only here).
+__global__ void __launch_bounds__(256) k_shard_points(SampleParams P,
                                                       const unsigned* __restrict__ count,
+                                                      const int32_t* __restrict__ gid,
                                                       double2* __restrict__ pr) {
   const int64_t m = *count;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double r, p;
-    radius_from_u53((uint64_t)__double_as_longlong(pr[i].y), P, r, p);
-    pr[i].y = p;
+    double ph, r, p;
+    sample_point(__ldg(gid + i), P, ph, r, p);
+    pr[i] = make_double2(ph, p);
   }
 }
 
@@ -2367,9 +2358,38 @@ __global__ void k_queue_heavy_rows(QueryArgs A, const int64_t* __restrict__ rowp
 }
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,
-                                                double* __restrict__ s, double* __restrict__ c) {
+                                                double* __restrict__ s, double* __restrict__ c,
+                                                bool slow) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) sincos_cr(x[i], s + i, c + i);
+  if (i < n) {
+    if (slow) sincos_cr(x[i], s + i, c + i);
+    else sincos_crf(x[i], s + i, c + i);
+  }
+}
+
+// Fast path (with its rounding test) against the full double-double
+// evaluation on n Philox angles in [0, 2pi) plus, every 4th one, an angle
+// within 2^-20 of a multiple of pi/4: mismatches and fast-path rejections.
+__global__ void __launch_bounds__(256) k_sincos_compare(int64_t n, uint64_t seed,
+                                                        unsigned long long* __restrict__ out) {
+  unsigned long long bad = 0, slow = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t a, b;
+    philox_u53(i, seed, a, b);
+    double x = angle_from_u53(a);
+    if ((i & 3) == 3) {
+      const double m = (double)(b & 7) * 0.7853981633974483;
+      x = fabs(m + ((double)(a >> 20) * 0x1.0p-33 - 0.5) * 0x1.0p-19);
+    }
+    double s0, c0, s1, c1;
+    sincos_cr(x, &s0, &c0);
+    slow += !sincos_crf(x, &s1, &c1);
+    bad += (__double_as_longlong(s0) != __double_as_longlong(s1)) ||
+           (__double_as_longlong(c0) != __double_as_longlong(c1));
+  }
+  atomicAdd(out, bad);
+  atomicAdd(out + 1, slow);
 }
 
 __global__ void __launch_bounds__(256) k_widen(int64_t n, const int32_t* __restrict__ in,

@@ -142,6 +142,112 @@ __device__ __forceinline__ void sincos_cr(double x, double* s_out, double* c_out
   }
 }
 
+// ----------------------------------------- fast path with a rounding test
+// sin/cos of a = i/128, i in [-kScHalf, kScHalf], as double-doubles (hi, lo)
+// to ~2^-100, filled once per device by k_sincos_table from the same
+// double-double Taylor series as sincos_cr.
+constexpr int kScHalf = 101;                // 101/128 > pi/4 + the reduction's slack
+__device__ double4 g_sctab[2 * kScHalf + 1];  // (sin hi, sin lo, cos hi, cos lo)
+
+__global__ void k_sincos_table() {
+  const int i = threadIdx.x;
+  if (i > 2 * kScHalf) return;
+  const dd a = {(double)(i - kScHalf) * 0x1.0p-7, 0.0};
+  const dd s2 = dd_mul(a, a);
+  const dd sp = dd_mul(a, poly_dd<true>(s2));
+  const dd cp = poly_dd<false>(s2);
+  g_sctab[i] = make_double4(sp.hi, sp.lo, cp.hi, cp.lo);
+}
+
+// y = fl(v) for v = y + e (+- err), i.e. is y correctly rounded?  The
+// rounding interval of y is [y - dn/2, y + up/2] (dn != up at powers of 2).
+__device__ __forceinline__ bool rounds_to(double y, double e, double err) {
+  const double a = fabs(y);
+  if (!(a > 0.0)) return false;
+  const long long b = __double_as_longlong(a);
+  const double gap_up = __dsub_rn(__longlong_as_double(b + 1), a);  // above |y|
+  const double gap_dn = __dsub_rn(a, __longlong_as_double(b - 1));  // below |y|
+  const double up = y > 0.0 ? gap_up : gap_dn, dn = y > 0.0 ? gap_dn : gap_up;
+  return __dadd_rn(e, err) < __dmul_rn(0.5, up) && __dsub_rn(e, err) > __dmul_rn(-0.5, dn);
+}
+
+// sin/cos of x in [0, 2pi), correctly rounded.  Fast path: table value at
+// a = i/128 nearest to the reduced argument r, and the short series in
+// t = r - a (|t| <= 2^-8): sin r = S + C t + [S (cos t - 1) + C (sin t - t)],
+// cos r = C - S t + [C (cos t - 1) - S (sin t - t)], with the leading product
+// exact (fma) and the bracket (< 2^-16) in double.  Error of the bracket:
+// ten roundings of at most its magnitude A <= (|S| + |t|) t^2 / 2 (+ ulp-level
+// terms) give <= 2^-49.7 A, the omitted products (S_lo (cos t - 1), C_lo (sin
+// t - t)), the series' own roundings and truncations add < 2^-51 (|S| + |t|)
+// t^2, the table and the reduction < 2^-99: bounded by 2^-48 (|S| + |t|) t^2
+// + 2^-96 (C for S in the cosine).  A value whose rounding that error could
+// change (a few in 10^4) is recomputed by sincos_cr.
+__device__ __forceinline__ bool sincos_crf(double x, double* s_out, double* c_out) {
+  const double P1 = 0x1.921fb54400000p+0;
+  const double P2 = 0x1.0b4611a600000p-34;
+  const double P3 = 0x1.3198a2e000000p-69;
+  const double P4 = 0x1.b839a252049c1p-104;
+  const double kd = rint(__dmul_rn(x, 0x1.45f306dc9c883p-1));
+  const int k = (int)kd;
+  dd r = {__dsub_rn(x, __dmul_rn(kd, P1)), 0.0};
+  r = dd_add_d(r, -__dmul_rn(kd, P2));
+  r = dd_add_d(r, -__dmul_rn(kd, P3));
+  r = dd_add_d(r, -__dmul_rn(kd, P4));
+  const double fi = rint(__dmul_rn(r.hi, 128.0));
+  const int i = max(-kScHalf, min(kScHalf, (int)fi));
+  const double th = __dsub_rn(r.hi, __dmul_rn((double)i, 0x1.0p-7));  // exact (Sterbenz)
+  const double tl = r.lo;                                               // t = th + tl
+  const double4 T = g_sctab[i + kScHalf];
+  const double Sh = T.x, Sl = T.y, Ch = T.z, Cl = T.w;
+  // t^2 = t2 + t2e exactly for th; cross term 2 th tl
+  const double t2 = __dmul_rn(th, th);
+  const double t2e = fma(th, th, -t2);
+  const double txl = __dmul_rn(th, tl);
+  // cos t - 1 = -t^2/2 + t^4/24 - t^6/720  (t^8 term < 2^-71)
+  const double c4 = __dmul_rn(t2, __dsub_rn(1.0 / 24.0, __dmul_rn(t2, 1.0 / 720.0)));
+  const double cm1 = __dadd_rn(__dmul_rn(-0.5, t2),
+                               __dsub_rn(__dmul_rn(t2, c4), __dadd_rn(__dmul_rn(0.5, t2e), txl)));
+  // sin t - t = -t^3/6 + t^5/120 - t^7/5040  (t^9 term < 2^-80); d/dt: -t^2/2 tl
+  const double t3 = __dmul_rn(t2, th);
+  const double sp5 = __dmul_rn(t2, __dsub_rn(1.0 / 120.0, __dmul_rn(t2, 1.0 / 5040.0)));
+  const double sm = __dsub_rn(__dmul_rn(t3, __dsub_rn(sp5, 1.0 / 6.0)), __dmul_rn(0.5, __dmul_rn(t2, tl)));
+  // sin r
+  const double Ph = __dmul_rn(Ch, th), Pl = fma(Ch, th, -Ph);
+  const dd M = two_sum(Sh, Ph);
+  double sm_s = __dadd_rn(__dmul_rn(Cl, th), __dmul_rn(Ch, tl));
+  sm_s = __dadd_rn(sm_s, Pl);
+  sm_s = __dadd_rn(sm_s, Sl);
+  sm_s = __dadd_rn(sm_s, __dmul_rn(Ch, sm));
+  sm_s = __dadd_rn(sm_s, __dmul_rn(Sh, cm1));
+  sm_s = __dadd_rn(sm_s, M.lo);
+  const dd Ys = two_sum(M.hi, sm_s);
+  // cos r
+  const double Qh = __dmul_rn(Sh, th), Ql = fma(Sh, th, -Qh);
+  const dd N = two_sum(Ch, -Qh);
+  double sm_c = __dsub_rn(-__dmul_rn(Sl, th), __dmul_rn(Sh, tl));
+  sm_c = __dsub_rn(sm_c, Ql);
+  sm_c = __dadd_rn(sm_c, Cl);
+  sm_c = __dsub_rn(sm_c, __dmul_rn(Sh, sm));
+  sm_c = __dadd_rn(sm_c, __dmul_rn(Ch, cm1));
+  sm_c = __dadd_rn(sm_c, N.lo);
+  const dd Yc = two_sum(N.hi, sm_c);
+  double sr = Ys.hi, cr = Yc.hi;
+  const double at = fabs(th);
+  const double es = __dadd_rn(__dmul_rn(0x1.0p-48, __dmul_rn(t2, __dadd_rn(at, fabs(Sh)))), 0x1.0p-96);
+  const double ec = __dadd_rn(__dmul_rn(0x1.0p-48, __dmul_rn(t2, __dadd_rn(at, fabs(Ch)))), 0x1.0p-96);
+  if (!(rounds_to(Ys.hi, Ys.lo, es) && rounds_to(Yc.hi, Yc.lo, ec))) {
+    sincos_cr(x, s_out, c_out);
+    return false;
+  }
+  switch (k & 3) {
+    case 0: *s_out = sr; *c_out = cr; break;
+    case 1: *s_out = cr; *c_out = -sr; break;
+    case 2: *s_out = -sr; *c_out = -cr; break;
+    default: *s_out = -cr; *c_out = sr; break;
+  }
+  return true;
+}
+
 // ------------------------------------------------- reference arithmetic
 // hrgen geometry.py:149-157, literally: b=(1-rh)(1+rh); denom=a*b+2;
 // center_r=2*rh/denom; disc=center_r^2-(2*rh^2-a*b)/denom; rad=sqrt(disc).

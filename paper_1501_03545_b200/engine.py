@@ -163,6 +163,14 @@ class Engine:
                                             c.ctypes.data))
         return s, c
 
+    def debug_sincos_compare(self, n, seed=0):
+        """(mismatches, rejected) of the fast sin/cos against the full one."""
+        mm = ctypes.c_int64()
+        rj = ctypes.c_int64()
+        _lib.check(self._L.hrg_debug_sincos_compare(self._ctx, int(n), ctypes.c_uint64(seed),
+                                                    ctypes.byref(mm), ctypes.byref(rj)))
+        return mm.value, rj.value
+
     def synchronize(self):
         _lib.check(self._L.hrg_synchronize(self._ctx))
 
