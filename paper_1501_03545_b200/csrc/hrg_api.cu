@@ -100,7 +100,7 @@ struct hrg_context {
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
-  int grid_light = 0, grid_light_wide = 0, grid_heavy = 0, grid_compact = 0;
+  int grid_light = 0, grid_light_wide = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
 namespace {
@@ -298,19 +298,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   }
 
   if (c->grid_light == 0) {
-    for (auto kern : {k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>,
-                      k_light<false, kSegCap, HRG_LIGHT_MINBLOCKS>})
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)light_smem<kSegCap>()));
-    for (auto kern : {k_light<true, kSegCapWide, 4>, k_light<false, kSegCapWide, 4>})
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)light_smem<kSegCapWide>()));
-    c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads,
-                                   light_smem<kSegCap>());
-    c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, 4>, kLightThreads,
-                                        light_smem<kSegCapWide>());
+    c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
+    c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, 4>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
-    // (k_compact_heavy shares the heavy grid: both walk the chunk list)
+    c->grid_compact_heavy = occupancy_grid(c, k_compact_heavy);
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSortWarpSmem));
@@ -373,11 +364,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     {
       constexpr int MB = HRG_LIGHT_MINBLOCKS;
-      const size_t sn = light_smem<kSegCap>(), sw = light_smem<kSegCapWide>();
-      if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, sn, st>>>(A);
-      else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, sn, st>>>(A);
-      else if (sample_ids) k_light<true, kSegCapWide, 4><<<gq, kLightThreads, sw, st>>>(A);
-      else k_light<false, kSegCapWide, 4><<<gq, kLightThreads, sw, st>>>(A);
+      if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (sample_ids) k_light<true, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);
+      else k_light<false, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);
     }
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
     k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),
@@ -432,7 +422,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
     k_scan_chunks<<<1, 1024, 0, st>>>(c->chunk_hits.as<int32_t>(), d_chunks,
                                       c->chunk_off.as<int64_t>(), A.overflow);
-    k_compact_heavy<<<c->grid_heavy, 256, 0, st>>>(A, 0, c->chunk_off.as<int64_t>(), rp, idx,
+    k_compact_heavy<<<c->grid_compact_heavy, 256, 0, st>>>(A, 0, c->chunk_off.as<int64_t>(), rp, idx,
                                                    sample_ids);
     if (sample_ids) k_queue_heavy_rows<<<2 * c->sm_count, 256, 0, st>>>(A, rp, J);
     CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));

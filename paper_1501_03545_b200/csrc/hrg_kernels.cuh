@@ -30,7 +30,7 @@ namespace hrg {
 
 // tuning knobs (-D overrides for experiments)
 #ifndef HRG_WALK_UNROLL
-#define HRG_WALK_UNROLL 2
+#define HRG_WALK_UNROLL 3
 #endif
 #ifndef HRG_BAND_GROUP
 #define HRG_BAND_GROUP 1
@@ -65,8 +65,14 @@ namespace hrg {
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 24
 #endif
+#ifndef HRG_HEAVY_MINB
+#define HRG_HEAVY_MINB 2
+#endif
+#ifndef HRG_HEAVY_BATCH
+#define HRG_HEAVY_BATCH 4
+#endif
 #ifndef HRG_LIGHT_MINBLOCKS
-#define HRG_LIGHT_MINBLOCKS 6
+#define HRG_LIGHT_MINBLOCKS 5
 #endif
 
 constexpr int kMaxBands = 32;     // one warp lane per radial band
@@ -1040,7 +1046,7 @@ constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | l
 // alpha: every band populated, so a light query holds up to 32 segments plus
 // wrap-around splits; with the narrow variant nearly all of them would be
 // deferred to the per-query heavy path).
-constexpr int kSegCapWide = 40;
+constexpr int kSegCapWide = 36;   // static shared memory stays under 48 KB
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
 struct LightSmem {
@@ -1063,8 +1069,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
   constexpr int kSegCap = kCap;
   constexpr int kSegStride = LightSmem<kCap>::kStride;
   __shared__ Band sb[kMaxBands];
-  extern __shared__ __align__(16) unsigned char light_dyn[];
-  LightSmem<kCap>& sm = *reinterpret_cast<LightSmem<kCap>*>(light_dyn);
+  __shared__ LightSmem<kCap> sm;  // static: compile-time shared addresses
   load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -1383,7 +1388,8 @@ __global__ void __launch_bounds__(1024) k_scan_chunks(const int32_t* __restrict_
 // at a time (4 batches in flight) with ballot-ordered writes into the
 // chunk's slot of the query's staging slice.
 template <bool kSampleIds>
-__global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
+__global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int64_t H) {
+  constexpr int HB = HRG_HEAVY_BATCH;  // batches of 32 candidates in flight
   if (*A.overflow) return;  // void pass, re-run by the host
   __shared__ Band sb[kMaxBands];
   if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
@@ -1418,11 +1424,11 @@ __global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
     int32_t* out = A.stage + slot;
     const bool fits = slot + (end - beg) <= A.stage_cap;
     int32_t hits = 0;
-    for (int32_t base = beg; base < end; base += 128) {
-      int32_t wv[4];
-      bool ok[4];
+    for (int32_t base = beg; base < end; base += 32 * HB) {
+      int32_t wv[HB];
+      bool ok[HB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < HB; ++u) {
         int32_t i = base + 32 * u + lane;
         int o = 0;
 #pragma unroll
@@ -1437,12 +1443,12 @@ __global__ void __launch_bounds__(256, 3) k_heavy(QueryArgs A, int64_t H) {
         wv[u] = tt < la ? sa + tt : sbb + (tt - la);
         ok[u] = i < end;
       }
-      Cand r[4];
+      Cand r[HB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < HB; ++u)
         if (ok[u]) r[u] = load_cand<kSampleIds>(A, f, wv[u]);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < HB; ++u) {
         bool hit = ok[u] && pair_test(f, r[u], wv[u]);
         unsigned bal = __ballot_sync(FULL, hit);
         if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = r[u].id;
