@@ -434,9 +434,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       CUDA_TRY(c->idx2.ensure(4 * (size_t)cap));
       const RowList none{nullptr, nullptr, nullptr};
       const unsigned sm = (unsigned)c->sm_count;
-      k_sort_warp<<<8 * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
+      k_sort_warp<<<HRG_SORT_GRID * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
       k_sort_rows<256, kBucketMax, kMidShift>
-          <<<8 * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(idx, idx, J.mid, J.large);
+          <<<HRG_SORT_GRID * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(idx, idx, J.mid,
+                                                                                J.large);
       k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
           idx, idx, J.large, G.rows);
       k_giant_plan<<<1, 1024, 0, st>>>(G);

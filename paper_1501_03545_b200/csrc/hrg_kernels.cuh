@@ -33,7 +33,7 @@ namespace hrg {
 #define HRG_WALK_UNROLL 3
 #endif
 #ifndef HRG_BAND_GROUP
-#define HRG_BAND_GROUP 1
+#define HRG_BAND_GROUP 2
 #endif
 #ifndef HRG_SMALL_SLOTS
 #define HRG_SMALL_SLOTS 64
@@ -63,7 +63,13 @@ namespace hrg {
 #define HRG_COMPACT_MINB 5
 #endif
 #ifndef HRG_SEGCAP
-#define HRG_SEGCAP 24
+#define HRG_SEGCAP 28
+#endif
+#ifndef HRG_SORTWARP_MINB
+#define HRG_SORTWARP_MINB 6
+#endif
+#ifndef HRG_SORT_GRID
+#define HRG_SORT_GRID 12
 #endif
 #ifndef HRG_HEAVY_MINB
 #define HRG_HEAVY_MINB 2
@@ -1041,7 +1047,7 @@ constexpr int kFirstSeg = 1 << 30;            // flat entry: the query's first s
 constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | lane
 
 // Per-lane segment slots (kCap + 1 stride, padded against bank conflicts).
-// Two variants: kSegCap slots at 6 blocks/SM, and kSegCapWide slots at 4
+// Two variants: kSegCap slots at 5 blocks/SM, and kSegCapWide slots at 4
 // blocks/SM for models whose queries reach most of the 32 bands (small
 // alpha: every band populated, so a light query holds up to 32 segments plus
 // wrap-around splits; with the narrow variant nearly all of them would be
@@ -1947,7 +1953,7 @@ __device__ __forceinline__ void lane_sort_bucket(int32_t* b, int32_t c) {
 // Queued rows (sample-order ids), one warp per row: up to 64 ids by a
 // register network, up to kWarpBucketMax by a bucket sort in shared memory;
 // longer rows go on to k_sort_rows.
-__global__ void __launch_bounds__(kSortWarpThreads, 4) k_sort_warp(int32_t* __restrict__ idx,
+__global__ void __launch_bounds__(kSortWarpThreads, HRG_SORTWARP_MINB) k_sort_warp(int32_t* __restrict__ idx,
                                                                 SortJobs J) {
   extern __shared__ __align__(16) unsigned char sort_smem[];
   SortWarpSmem& S = reinterpret_cast<SortWarpSmem*>(sort_smem)[threadIdx.x >> 5];
