@@ -65,6 +65,9 @@ namespace hrg {
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 28
 #endif
+#ifndef HRG_TILE_HITS
+#define HRG_TILE_HITS 2048
+#endif
 #ifndef HRG_SORTWARP_MINB
 #define HRG_SORTWARP_MINB 6
 #endif
@@ -1640,7 +1643,7 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
 constexpr int kCompactThreads = 128;
 constexpr bool kElemWrite = HRG_ELEM_WRITE;  // compaction writes rows element-parallel
 constexpr int kSmallSlots = HRG_SMALL_SLOTS;    // rows sorted by one thread (32 or 64)
-constexpr int kTileHits = 2048;                 // smem hits per warp
+constexpr int kTileHits = HRG_TILE_HITS;                 // smem hits per warp
 constexpr int kCopyUnroll = 8;                  // loads in flight per lane
 
 // 4-byte global -> shared copy that bypasses registers (LDGSTS).
@@ -1683,16 +1686,15 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
     const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
     const bool active = v0 < (int32_t)(tv >> 32);
     const int32_t v = active ? v0 : 0;
-    const bool light = active && A.heavy_of[v] < 0;
-    int32_t ns = 0, len = 0;
-    int64_t dst = 0, src = INT64_MAX;
-    if (light) {
-      const int32_t idv = kSampleIds ? __ldg(A.rec.ids + v) : v;
-      dst = rowptr[idv];
-      len = (int32_t)(rowptr[idv + 1] - dst);
-      ns = A.slots[v];
-      src = A.stage_off[v];
-    }
+    // independent loads first (one round trip), then the row's CSR offset;
+    // a light row's length is its hit count k_light left in slots[]
+    const int32_t hv = active ? A.heavy_of[v] : 0;
+    const int32_t idv = active ? (kSampleIds ? __ldg(A.rec.ids + v) : v) : 0;
+    const int32_t sl = active ? A.slots[v] : 0;
+    const int64_t so = active ? A.stage_off[v] : INT64_MAX;
+    const bool light = active && hv < 0;
+    const int32_t ns = light ? sl : 0, len = ns;
+    const int64_t dst = light ? rowptr[idv] : 0, src = light ? so : INT64_MAX;
     int64_t base = src;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) base = min(base, (int64_t)__shfl_xor_sync(FULL, base, o));
