@@ -100,7 +100,7 @@ struct hrg_context {
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
-  int grid_light = 0, grid_light_wide = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
+  int grid_light = 0, grid_light_wide = 0, grid_light_shard = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
 namespace {
@@ -300,6 +300,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   if (c->grid_light == 0) {
     c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, 4>, kLightThreads);
+    c->grid_light_shard =
+        occupancy_grid(c, k_light<true, kSegCapShard, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact_heavy = occupancy_grid(c, k_compact_heavy);
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
@@ -327,8 +329,14 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     wide = populated >= kWideBands;
     if (const char* e = getenv("HRG_LIGHT_WIDE")) wide = atoi(e) != 0;
   }
+  // a sharded run has ~8x fewer tiles per warp, and there the 4 extra slots
+  // of kSegCap cost more in the light pass (measured: 0.49 -> 0.69 ms per
+  // rank at config 2, N = 8) than the deferrals they save
+  const bool shard_slots = !wide && np < n;
   unsigned gq = (unsigned)std::max<int64_t>(
-      1, std::min<int64_t>(blocks_for(np, kLightThreads), wide ? c->grid_light_wide : c->grid_light));
+      1, std::min<int64_t>(blocks_for(np, kLightThreads),
+                           wide ? c->grid_light_wide
+                                : (shard_slots ? c->grid_light_shard : c->grid_light)));
   unsigned gc = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
@@ -364,7 +372,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     {
       constexpr int MB = HRG_LIGHT_MINBLOCKS;
-      if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      if (sample_ids && shard_slots)
+        k_light<true, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (shard_slots) k_light<false, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (sample_ids) k_light<true, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);
       else k_light<false, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);

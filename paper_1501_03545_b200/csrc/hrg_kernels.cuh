@@ -1056,6 +1056,7 @@ constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | l
 // wrap-around splits; with the narrow variant nearly all of them would be
 // deferred to the per-query heavy path).
 constexpr int kSegCapWide = 36;   // static shared memory stays under 48 KB
+constexpr int kSegCapShard = 24;  // sharded runs (few tiles per warp)
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
 struct LightSmem {

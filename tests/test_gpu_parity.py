@@ -170,6 +170,23 @@ def test_generate_matches_oracle(oracle, kw):
     assert len(diff) <= max(2, g.m // 1_000_000)
 
 
+@pytest.mark.parametrize("wide", ["0", "1"])
+@pytest.mark.parametrize("kw", [GEN_CASES[1], GEN_CASES[2], GEN_CASES[5]],
+                         ids=["k32-g2.5", "k4-g2.2", "R35.5"])
+def test_light_query_variants_match_oracle(oracle, kw, wide, monkeypatch):
+    """Both light-query variants (28 and 36 segment slots; the model picks
+    one, HRG_LIGHT_WIDE forces it) give the oracle's edge set exactly."""
+    monkeypatch.setenv("HRG_LIGHT_WIDE", wide)
+    p = GeneratorParams(**kw)
+    model = p.resolve()
+    g = P.generate(p)
+    co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                    P.to_poincare_radius(model.R), 512, oracle.TRIG_CR)
+    assert g.m == m and np.array_equal(g.edge_array(), e)
+
+
 def test_config1_full_size_matches_oracle(oracle):
     """BASELINE config 1 (n=1e6, k=10, gamma=3, seed 1) end to end."""
     p = GeneratorParams(n=1_000_000, avg_degree=10.0, gamma=3.0, seed=1)
