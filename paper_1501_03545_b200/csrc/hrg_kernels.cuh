@@ -757,7 +757,7 @@ __global__ void k_shard_prep(SampleParams P, ShardSample S,
 // order of kept points is arbitrary: ties of the 32-bit sort key may land in
 // any order, which changes no row (rows are sorted by id) and no window
 // (exact trims hold on any order).
-constexpr int kShardPer = 8;
+constexpr int kShardPer = 16;
 __global__ void __launch_bounds__(256) k_shard_select(int64_t n, int L,
                                                       const uint32_t* __restrict__ keys_all,
                                                       const int64_t* __restrict__ lo,
@@ -768,26 +768,34 @@ __global__ void __launch_bounds__(256) k_shard_select(int64_t n, int L,
                                                       int32_t* __restrict__ gid,
                                                       unsigned* __restrict__ count) {
   __shared__ unsigned wcnt[8], wbase[8], bbase;
-  __shared__ int64_t s_lo[kMaxBands], s_hi[kMaxBands];
-  __shared__ int s_mode[kMaxBands];
+  // per band: (lo, hi | (mode + 1) << 28) in 27-bit angle units, one load
+  __shared__ uint2 s_rng[kMaxBands];
   if (threadIdx.x < kMaxBands) {
     const int j = threadIdx.x;
-    s_lo[j] = j < L ? lo[j] : 0;
-    s_hi[j] = j < L ? hi[j] : 0;
-    s_mode[j] = j < L ? mode[j] : -1;
+    const int md = j < L ? mode[j] : -1;
+    s_rng[j] = make_uint2(md == 0 ? (unsigned)lo[j] : 0u,
+                          (md == 0 ? (unsigned)hi[j] : 0u) | ((unsigned)(md + 1) << 28));
   }
   __syncthreads();
+  auto keep_of = [&](uint32_t k) {
+    const uint2 g = s_rng[k >> 27];
+    const unsigned q = k & ((1u << 27) - 1), h = g.y & 0x0fffffffu;
+    const int md = (int)(g.y >> 28) - 1;
+    return md > 0 || (md == 0 && (g.x <= h ? (q >= g.x && q < h) : (q >= g.x || q < h)));
+  };
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t i0 = (int64_t)blockIdx.x * (256 * kShardPer) + threadIdx.x;
   uint32_t kk[kShardPer];
   unsigned ballots[kShardPer];
   unsigned warp_tot = 0;
 #pragma unroll
-  for (int k = 0; k < kShardPer; ++k) {
+  for (int k = 0; k < kShardPer; ++k) {  // all loads in flight first
     const int64_t i = i0 + 256 * k;
     kk[k] = i < n ? __ldg(keys_all + i) : 0u;
-    const bool keep = i < n && shard_keep((int)(kk[k] >> 27), (int64_t)(kk[k] & ((1u << 27) - 1)),
-                                          s_lo, s_hi, s_mode);
+  }
+#pragma unroll
+  for (int k = 0; k < kShardPer; ++k) {
+    const bool keep = i0 + 256 * k < n && keep_of(kk[k]);
     ballots[k] = __ballot_sync(0xffffffffu, keep);
     warp_tot += __popc(ballots[k]);
   }
