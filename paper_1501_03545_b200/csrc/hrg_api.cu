@@ -75,7 +75,7 @@ struct hrg_context {
   // sort
   Buf keys_out, vals_in, vals_out;
   // sorted records
-  Buf pt, circ, rec, s_phi, s_rf, s_bf, s_rp, s_rn, pr;
+  Buf pt, circ, rec, s_phi, s_rf, s_rp, s_rn, pr;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits, chunk_entry,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
@@ -145,7 +145,7 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(128));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
   CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
-  CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_bf.ensure(f));
+  CUDA_TRY(c->s_rf.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
   CUDA_TRY(c->dir.ensure(4 * (size_t)((2 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->dir_total.ensure(16)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
@@ -176,7 +176,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                                            c->k32_out.as<uint32_t>(), c->vals_in.as<int32_t>(),
                                            c->vals_out.as<int32_t>(), (int)n, 0, 32, st));
   CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
-  QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
+  QRec q{c->s_phi.as<double>(), c->s_rf.as<float>()};
   const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
                   c->vals_out.as<int32_t>()};
   if (sample_ids)
@@ -203,9 +203,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr);
   k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(
-      n, c->keys_out.as<uint64_t>(), c->s_rf.as<float>(), c->s_bf.as<float>(),
-      c->s_rp.as<double>(), c->bands.as<Band>());
-  k_band_finish<<<1, 64, 0, st>>>(c->bands.as<Band>(), L);
+      n, c->keys_out.as<uint64_t>(), c->s_rp.as<double>(), c->bands.as<Band>());
   CUDA_TRY(c->dir_gaps.ensure(sizeof(DirGap) * (size_t)(n / 16 + 2 * kMaxBands + 8)));
   unsigned* ngaps = reinterpret_cast<unsigned*>(c->dir_total.as<char>() + 8);
   CUDA_TRY(cudaMemsetAsync(ngaps, 0, 4, st));
@@ -254,7 +252,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   memset(&A, 0, sizeof(A));
   A.rec = Recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
                 c->vals_out.as<int32_t>()};
-  A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_bf.as<float>()};
+  A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>()};
   A.bands = c->bands.as<Band>();
   A.dir = c->dir.as<int32_t>();
   A.keys = c->keys_out.as<uint64_t>();
@@ -735,7 +733,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_bf, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
+                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_entry, &c->chunk_off,
                  &c->slots,

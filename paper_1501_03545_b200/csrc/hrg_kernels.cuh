@@ -95,10 +95,6 @@ struct Band {
   int64_t dir_base;        // offset of the band's directory in dir[]
   int32_t shift;           // bucket(q) = q >> shift
   int32_t nb;              // buckets (power of two); directory has nb + 1 entries
-  float rmin;              // min hyperbolic radius 2*atanh(r_poincare) in band (rounded down)
-  float bmin;              // min (1-r)(1+r) in band (rounded down)
-  float sinh_rmin;
-  float pad_;
   double pmin;             // innermost Poincare radius of the band's points
 };
 
@@ -259,8 +255,7 @@ struct Recs {
 
 struct QRec {          // query-side extras, per sorted position
   double* phi;
-  float* rf;           // hyperbolic radius 2*atanh(r) (rounded down)
-  float* bf;           // (1-r)(1+r) (rounded down)
+  float* rf;           // a lower bound of the hyperbolic radius 2*atanh(r)
 };
 
 // Gather into (band, angle) order and precompute every per-point quantity the
@@ -307,12 +302,13 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
     rec.circ[p] = ci;
   }
   q.phi[p] = ph;
-  // hyperbolic radius of the stored Poincare point and (1-r)(1+r), both
-  // rounded down: only used to size conservative angular windows.
-  double one_m = 1.0 - r;
-  double re = log1p(2.0 * r / one_m);  // 2*atanh(r)
-  q.rf[p] = __double2float_rd(re);
-  q.bf[p] = __double2float_rd(one_m * (1.0 + r));
+  // a lower bound of the hyperbolic radius of the stored Poincare point,
+  // only used to pick the window-table row (a smaller radius picks a row
+  // of wider windows): 2 atanh(r) = log((1 + r)/(1 - r)) in float, with
+  // 1 - r exact in double (r <= 1 - 2^-53), then 1e-5 relative and 1e-5
+  // absolute taken off (float log and division err by < 1e-6 relative)
+  const float lr = __logf(__fdividef((float)(1.0 + r), (float)(1.0 - r)));
+  q.rf[p] = fmaxf(0.0f, lr * (1.0f - 1e-5f) - 1e-5f);
   if (s_rp) s_rp[p] = r;
   if (s_rn) s_rn[p] = rn[i];
 }
@@ -351,10 +347,7 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     lg = min(lg + kDirExtra, kQBits - kSortShift);                // (x 2^kDirExtra)
     B.nb = 1 << lg;
     B.shift = kQBits - lg;
-    B.rmin = __int_as_float(0x7f800000);
-    B.bmin = __int_as_float(0x7f800000);
-    B.sinh_rmin = 0.f;
-    B.pad_ = 0.f;
+
     B.pmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf until k_band_minmax
     B.dir_base = 0;
     bands[j] = B;
@@ -367,46 +360,34 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
   }
 }
 
-// Per-band min radius / min (1-r)(1+r): a block reduces its (few) bands in
-// shared memory, then one atomicMin per band per block on the bit patterns of
-// positive floats (order-preserving, so deterministic).
+// Innermost Poincare radius of each band's points.  Sorted positions: a
+// warp's 32 points are nearly always one band, reduced in registers.
 __global__ void __launch_bounds__(256) k_band_minmax(int64_t n, const uint64_t* __restrict__ keys,
-                                                     const float* __restrict__ rf,
-                                                     const float* __restrict__ bf,
                                                      const double* __restrict__ s_rp,
                                                      Band* __restrict__ bands) {
-  __shared__ int sr[kMaxBands], sbm[kMaxBands];
   __shared__ unsigned long long sp[kMaxBands];
-  if (threadIdx.x < kMaxBands) {
-    sr[threadIdx.x] = 0x7f800000; sbm[threadIdx.x] = 0x7f800000;
-    sp[threadIdx.x] = 0x7ff0000000000000ull;
-  }
+  if (threadIdx.x < kMaxBands) sp[threadIdx.x] = 0x7ff0000000000000ull;
   __syncthreads();
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int band = (int)(keys[p] >> kQBits);
-    const int r = __float_as_int(rf[p]), b = __float_as_int(bf[p]);
-    const unsigned same = __match_any_sync(__activemask(), band);
-    const int rm = (int)__reduce_min_sync(same, (unsigned)r);
-    const int bm = (int)__reduce_min_sync(same, (unsigned)b);
-    if ((threadIdx.x & 31) == __ffs(same) - 1) {
-      atomicMin(&sr[band], rm);
-      atomicMin(&sbm[band], bm);
-    }
+  const unsigned FULL = 0xffffffffu;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x; p0 < n; p0 += stride) {
+    const int64_t p = p0 + threadIdx.x;
+    const bool ok = p < n;
+    const int band = ok ? (int)(keys[p] >> kQBits) : -1;
     // non-negative doubles order like their bit patterns
-    atomicMin(&sp[band], (unsigned long long)__double_as_longlong(s_rp[p]));
+    unsigned long long v = ok ? (unsigned long long)__double_as_longlong(s_rp[p]) : ~0ull;
+    const int b0 = __shfl_sync(FULL, band, 0);
+    if (__all_sync(FULL, band == b0)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+      if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicMin(&sp[b0], v);
+    } else if (ok) {
+      atomicMin(&sp[band], v);
+    }
   }
   __syncthreads();
-  if (threadIdx.x < kMaxBands && sr[threadIdx.x] != 0x7f800000) {
-    atomicMin((int*)&bands[threadIdx.x].rmin, sr[threadIdx.x]);
-    atomicMin((int*)&bands[threadIdx.x].bmin, sbm[threadIdx.x]);
+  if (threadIdx.x < kMaxBands && sp[threadIdx.x] != 0x7ff0000000000000ull)
     atomicMin(reinterpret_cast<unsigned long long*>(&bands[threadIdx.x].pmin), sp[threadIdx.x]);
-  }
-}
-
-__global__ void k_band_finish(Band* bands, int L) {
-  int j = threadIdx.x;
-  if (j < L) bands[j].sinh_rmin = sinhf(bands[j].rmin);
 }
 
 // dir[base + k] = first position of the band whose bucket >= k.
