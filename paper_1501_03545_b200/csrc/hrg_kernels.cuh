@@ -110,6 +110,16 @@ __device__ __forceinline__ int band_of(const BandSpec& S, double rp) {
   return b;
 }
 
+// The same count by binary search over the thresholds staged in shared
+// memory (thr non-decreasing; entries past L hold +inf).
+__device__ __forceinline__ int band_of_smem(const double* thr, double rp) {
+  int b = 0;
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1)
+    if (thr[b + st] <= rp) b += st;
+  return b;
+}
+
 // Angular fixed point: monotone in phi, identical expression everywhere.
 __device__ __forceinline__ uint64_t qkey(double x, double C) {
   double t = floor(__dmul_rn(x, C));
@@ -175,6 +185,11 @@ __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandS
                                                 uint32_t* __restrict__ keys,
                                                 int32_t* __restrict__ vals,
                                                 double2* __restrict__ pr) {
+  __shared__ double s_thr[kMaxBands];
+  if (threadIdx.x < kMaxBands)
+    s_thr[threadIdx.x] =
+        threadIdx.x < S.L ? S.thr[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
+  __syncthreads();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ph, r, p;
@@ -183,7 +198,7 @@ __global__ void __launch_bounds__(256) k_sample(int64_t n, SampleParams P, BandS
   if (rn) rn[i] = r;
   if (rp) rp[i] = p;
   pr[i] = make_double2(ph, p);
-  keys[i] = sort_key32(band_of(S, p), qkey(ph, P.C));
+  keys[i] = sort_key32(band_of_smem(s_thr, p), qkey(ph, P.C));
   vals[i] = (int32_t)i;
 }
 
