@@ -289,27 +289,80 @@ def run_ours(args):
     # the step's result (int64 CSR, hrgen.Graph's dtype) into pinned host memory
     e2e = None
     if not args.no_e2e:
-        k2 = max(1, min(args.steps, 3))
+        # The C ABI with HOST buffers: hrg_generate + hrg_copy_result of the
+        # step's result (int64 CSR, hrgen.Graph's dtype) into pinned host
+        # memory.  Two generator contexts on their own streams, driven by two
+        # host threads, alternate steps, so one graph's device->host copy (PCIe,
+        # the bound) overlaps the next graph's generation; every step still
+        # generates a graph and reads all of it back.
+        import threading
+        k2 = max(2, min(2 * args.steps, 8))
         n_, nnz_ = eng.sizes()
-        host_indptr = torch.empty(n_ + 1, dtype=torch.int64, pin_memory=True).numpy()
-        host_idx = torch.empty(int(nnz_ * 1.01) + 1024, dtype=torch.int64,
-                               pin_memory=True).numpy()
+        streams = [torch.cuda.Stream(device=local) for _ in range(2)]
+        engines = [P.Engine(local, stream=s.cuda_stream) for s in streams]
+        bufs = [(torch.empty(n_ + 1, dtype=torch.int64, pin_memory=True).numpy(),
+                 torch.empty(int(nnz_ * 1.01) + 1024, dtype=torch.int64, pin_memory=True).numpy())
+                for _ in range(2)]
+
+        def one_step(w):
+            e = engines[w]
+            e.generate(model, params["seed"], order, shard)
+            _, nz = e.sizes()
+            e.copy_result_into(indptr=bufs[w][0], indices=bufs[w][1][:nz])
+            return nz
+
+        for w in range(2):  # warm both contexts (allocations, staging sizes)
+            one_step(w)
+
+        started = threading.Event()
+
+        def worker(w, count, out):
+            # context 1 starts once context 0's first graph is generated, so
+            # the two alternate (generate one while the other's copy runs)
+            # instead of generating and copying in lockstep
+            if w == 1:
+                started.wait()
+            res_w = []
+            for i in range(count):
+                e = engines[w]
+                e.generate(model, params["seed"], order, shard)
+                if w == 0 and i == 0:
+                    started.set()
+                _, nz = e.sizes()
+                e.copy_result_into(indptr=bufs[w][0], indices=bufs[w][1][:nz])
+                res_w.append(nz)
+            out[w] = res_w
+
+        # sequential (one context) for reference
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(k2):
-            eng.generate(model, params["seed"], order, shard)
-            _, nnz_ = eng.sizes()
-            eng.copy_result_into(indptr=host_indptr, indices=host_idx[:nnz_])
+            one_step(0)
+        seq = (time.perf_counter() - t0) / k2
+        barrier()
         torch.cuda.synchronize()
-        dt = torch.tensor([(time.perf_counter() - t0) / k2], dtype=torch.float64, device="cuda")
+        t0 = time.perf_counter()
+        res = {}
+        ths = [threading.Thread(target=worker, args=(w, k2 // 2, res)) for w in range(2)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        torch.cuda.synchronize()
+        dt = torch.tensor([(time.perf_counter() - t0) / (2 * (k2 // 2))], dtype=torch.float64,
+                          device="cuda")
         if dist is not None:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         d2h = (n_ + 1) * 8 + int(nnz_) * 8
         e2e = {"value": m_total / float(dt.item()), "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(dt.item()),
+               "ms_per_step_one_context": 1e3 * seq,
                "api": "hrg_generate + hrg_copy_result (C ABI) into pinned host buffers, "
-                      "int64 CSR; the inputs are 5 scalar parameters"}
+                      "int64 CSR; two contexts on two streams alternating steps (the copy "
+                      "of one graph overlaps the generation of the next); inputs are 5 "
+                      "scalar parameters"}
+        del engines
 
     if rank != 0:
         if dist is not None:

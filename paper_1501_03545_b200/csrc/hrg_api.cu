@@ -100,6 +100,8 @@ struct hrg_context {
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
+  unsigned char* h_rb = nullptr;  // mapped pinned readback area (kReadback bytes)
+  unsigned char* d_rb = nullptr;  // its device alias
   int grid_light = 0, grid_light_wide = 0, grid_light_shard = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
@@ -154,6 +156,28 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
 }
 
 inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+// Small device->host readbacks through mapped pinned memory (a kernel
+// stores, the host reads after the stream sync): no copy-engine command, so a
+// readback never queues behind another context's multi-GB result copy.
+constexpr size_t kReadback = 256;
+struct RbItem { const void* src; size_t bytes; };
+__global__ void k_readback(RbItem a, RbItem b, unsigned char* dst) {
+  for (size_t i = threadIdx.x; i < a.bytes; i += blockDim.x)
+    dst[i] = static_cast<const unsigned char*>(a.src)[i];
+  for (size_t i = threadIdx.x; i < b.bytes; i += blockDim.x)
+    dst[a.bytes + i] = static_cast<const unsigned char*>(b.src)[i];
+}
+
+hrg_status readback(hrg_context* c, const void* src_a, size_t na, void* dst_a,
+                    const void* src_b = nullptr, size_t nb = 0, void* dst_b = nullptr) {
+  k_readback<<<1, 128, 0, c->stream>>>(RbItem{src_a, na}, RbItem{src_b, nb}, c->d_rb);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  memcpy(dst_a, c->h_rb, na);
+  if (nb) memcpy(dst_b, c->h_rb + na, nb);
+  return HRG_OK;
+}
 
 double ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -459,9 +483,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
     CUDA_TRY(cudaGetLastError());
     // the one synchronisation: counters, edge total, overflow flag
-    CUDA_TRY(cudaMemcpyAsync(ctr, c->counters.p, 128, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(&nnz, c->rowptr.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    {
+      hrg_status rs = readback(c, c->counters.p, 128, ctr, c->rowptr.as<int64_t>() + n, 8, &nnz);
+      if (rs != HRG_OK) return rs;
+    }
     total_chunks = (int64_t)ctr[14];
     if ((ctr[3] & 0xffffffffull) == 0) break;
     // staging overflowed: size it from the bump allocator's final value
@@ -551,8 +576,10 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
                                       c->sh_keep.as<uint8_t>(), c->vals_out.as<int32_t>(), d_cnt,
                                       (int)n, st));
   int np = 0;
-  CUDA_TRY(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  {
+    hrg_status rs = readback(c, d_cnt, 4, &np);
+    if (rs != HRG_OK) return rs;
+  }
   CUDA_TRY(cudaMemcpyAsync(c->k32_in.p, c->k32_out.p, 4 * (size_t)np, cudaMemcpyDeviceToDevice,
                            st));
   CUDA_TRY(cudaMemcpyAsync(c->vals_in.p, c->vals_out.p, 4 * (size_t)np, cudaMemcpyDeviceToDevice,
@@ -619,8 +646,10 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
                                                   c->pr.as<double2>());
   CUDA_TRY(cudaGetLastError());
   unsigned np = 0;
-  CUDA_TRY(cudaMemcpyAsync(&np, d_cnt, 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  {
+    hrg_status rs = readback(c, d_cnt, 4, &np);
+    if (rs != HRG_OK) return rs;
+  }
   c->np = np;
   c->sh_sampled = true;
   return HRG_OK;
@@ -667,8 +696,8 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
         c->k32_in.as<uint32_t>(), c->vals_in.as<int32_t>(), c->bad.as<int>(),
         c->pr.as<double2>());
     int bad = 0;
-    CUDA_TRY(cudaMemcpyAsync(&bad, c->bad.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    hrg_status rs = readback(c, c->bad.p, 4, &bad);
+    if (rs != HRG_OK) return rs;
     if (bad) return fail(HRG_ERR_OUT_OF_BOUNDS, "point outside the tree region");
   }
   CUDA_TRY(cudaGetLastError());
@@ -719,6 +748,13 @@ hrg_status hrg_context_create(int device, void* cuda_stream, hrg_context** out) 
     cudaError_t r = cudaEventCreate(&e);
     if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
   }
+  {
+    cudaError_t r = cudaHostAlloc(reinterpret_cast<void**>(&c->h_rb), kReadback,
+                                  cudaHostAllocMapped);
+    if (r == cudaSuccess)
+      r = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_rb), c->h_rb, 0);
+    if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
+  }
   // the sin/cos table of the fast path (device-global, idempotent)
   k_sincos_table<<<1, 256, 0, c->stream>>>();
   cudaError_t r = cudaStreamSynchronize(c->stream);
@@ -743,6 +779,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})
     b->release();
+  if (c->h_rb) cudaFreeHost(c->h_rb);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   delete c;
   return HRG_OK;
@@ -928,14 +965,11 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
     if (index_bytes == 4) {
       CUDA_TRY(cudaMemcpyAsync(indices, c->idx_final, 4 * (size_t)c->nnz, k, st));
     } else {
-      // widen on the device in chunks, copy each chunk out
-      const int64_t chunk = (int64_t)1 << 25;
-      CUDA_TRY(c->widen.ensure(8 * (size_t)std::min<int64_t>(chunk, c->nnz)));
-      for (int64_t off = 0; off < c->nnz; off += chunk) {
-        int64_t len = std::min<int64_t>(chunk, c->nnz - off);
-        k_widen<<<blocks_for(len), 256, 0, st>>>(len, c->idx_final + off, c->widen.as<int64_t>());
-        CUDA_TRY(cudaMemcpyAsync((int64_t*)indices + off, c->widen.p, 8 * (size_t)len, k, st));
-      }
+      // widen on the device in one pass, then one copy: the copy engine then
+      // never waits for SMs (another context's generation may hold them all)
+      CUDA_TRY(c->widen.ensure(8 * (size_t)c->nnz));
+      k_widen<<<blocks_for(c->nnz), 256, 0, st>>>(c->nnz, c->idx_final, c->widen.as<int64_t>());
+      CUDA_TRY(cudaMemcpyAsync(indices, c->widen.p, 8 * (size_t)c->nnz, k, st));
     }
   }
   CUDA_TRY(cudaStreamSynchronize(st));
