@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--vertex-order", default="sample", choices=("sample", "angular"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-queries", type=int, default=20_000,
+    ap.add_argument("--cpu-queries", type=int, default=100_000,
                     help="query vertices per CPU-baseline step (bounded sample)")
     ap.add_argument("--n", type=int, default=None, help="override the config's n")
     ap.add_argument("--k", type=float, default=None, help="override the config's avg degree")
