@@ -321,7 +321,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
 
   if (c->grid_light == 0) {
     c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
-    c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, 4>, kLightThreads);
+    c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, kWideMinBlocks>, kLightThreads);
     c->grid_light_shard =
         occupancy_grid(c, k_light<true, kSegCapShard, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
@@ -399,8 +399,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       else if (shard_slots) k_light<false, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (sample_ids) k_light<true, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);
-      else k_light<false, kSegCapWide, 4><<<gq, kLightThreads, 0, st>>>(A);
+      else if (sample_ids) k_light<true, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
+      else k_light<false, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
     }
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
     k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),

@@ -1059,7 +1059,14 @@ constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | l
 // alpha: every band populated, so a light query holds up to 32 segments plus
 // wrap-around splits; with the narrow variant nearly all of them would be
 // deferred to the per-query heavy path).
-constexpr int kSegCapWide = 36;   // static shared memory stays under 48 KB
+#ifndef HRG_WIDE_CAP
+#define HRG_WIDE_CAP 36
+#endif
+#ifndef HRG_WIDE_MINB
+#define HRG_WIDE_MINB 4
+#endif
+constexpr int kSegCapWide = HRG_WIDE_CAP;   // static shared memory stays under 48 KB
+constexpr int kWideMinBlocks = HRG_WIDE_MINB;
 constexpr int kSegCapShard = 24;  // sharded runs (few tiles per warp)
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
