@@ -224,7 +224,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
     qlo <<= kSortShift;
     qhi <<= kSortShift;
   }
-  k_band_setup<<<1, 64, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
+  k_band_setup<<<1, 1024, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr);
   k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(
       n, c->keys_out.as<uint64_t>(), c->s_rp.as<double>(), c->bands.as<Band>());
@@ -548,7 +548,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   int64_t* hi = lo + kMaxBands;
   int* mode = reinterpret_cast<int*>(hi + kMaxBands);
   float* cover = reinterpret_cast<float*>(mode + kMaxBands);
-  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_min, sec_lo, sec_hi, lo,
+  k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_min, sec_lo, sec_hi, lo,
                                    hi, mode, cover);
   c->sh_cover = cover;
   c->sh_lo = lo;
@@ -631,7 +631,7 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
   int64_t* hi = lo + kMaxBands;
   int* mode = reinterpret_cast<int*>(hi + kMaxBands);
   float* cover = reinterpret_cast<float*>(mode + kMaxBands);
-  k_shard_ranges<<<1, 32, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_pmin, S.sec_lo, S.sec_hi,
+  k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_pmin, S.sec_lo, S.sec_hi,
                                    lo, hi, mode, cover);
   c->sh_cover = cover;
   c->sh_lo = lo;

@@ -337,22 +337,59 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n,
   return lo;
 }
 
+// Warp-cooperative lower bound: 32 probes per step, so ~log32(n) dependent
+// loads instead of log2(n) (each a DRAM round trip on a cold array).
+__device__ __forceinline__ int64_t warp_lower_bound_u64(const uint64_t* a, int64_t n, uint64_t key,
+                                                        int lane) {
+  const unsigned FULL = 0xffffffffu;
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + (int64_t)lane * step;
+    const bool pred = p < hi && a[p] < key;
+    const int c = __popc(__ballot_sync(FULL, pred));
+    if (c == 0) return lo;
+    const int64_t nlo = lo + (int64_t)(c - 1) * step + 1;
+    const int64_t nhi = min(hi, lo + (int64_t)c * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  const int64_t p = lo + lane;
+  const bool pred = p < hi && a[p] < key;
+  return lo + __popc(__ballot_sync(FULL, pred));
+}
+
 // One block: band position ranges, shard query ranges, directory sizing.
 __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L,
                              uint64_t qsec_lo, uint64_t qsec_hi, Band* __restrict__ bands,
                              int64_t* __restrict__ dir_total,
                              const float* __restrict__ cover) {
-  __shared__ int64_t st[kMaxBands + 1];
-  int j = threadIdx.x;
-  if (j <= L) st[j] = lower_bound_u64(keys, n, (uint64_t)j << kQBits);
+  // searches by warp (block of 32 warps): band starts, then sector bounds
+  __shared__ int64_t st[kMaxBands + 1], sq0[kMaxBands], sq1[kMaxBands];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = w; t < 3 * (kMaxBands + 1); t += nw) {
+    const int which = t / (kMaxBands + 1), b = t % (kMaxBands + 1);
+    if (b > L || (which > 0 && b >= L)) continue;
+    const uint64_t base = (uint64_t)b << kQBits;
+    if (which == 0) {
+      const int64_t r = warp_lower_bound_u64(keys, n, base, lane);
+      if (lane == 0) st[b] = r;
+    } else if (which == 1) {
+      const int64_t r = warp_lower_bound_u64(keys, n, base | qsec_lo, lane);
+      if (lane == 0) sq0[b] = r;
+    } else if (qsec_hi <= kQMask) {
+      const int64_t r = warp_lower_bound_u64(keys, n, base | qsec_hi, lane);
+      if (lane == 0) sq1[b] = r;
+    }
+  }
   __syncthreads();
+  const int j = threadIdx.x;
   if (j < L) {
     Band B;
     B.start = (int32_t)st[j];
     B.end = (int32_t)st[j + 1];
-    uint64_t base = (uint64_t)j << kQBits;
-    B.qstart = (int32_t)lower_bound_u64(keys, n, base | qsec_lo);
-    B.qend = qsec_hi > kQMask ? B.end : (int32_t)lower_bound_u64(keys, n, base | qsec_hi);
+    B.qstart = (int32_t)sq0[j];
+    B.qend = qsec_hi > kQMask ? B.end : (int32_t)sq1[j];
     int64_t cnt = B.end - B.start;
     // a sharded run's subset covers only part of the circle: size the
     // directory for the band's density, not its count
@@ -639,14 +676,21 @@ __global__ void k_shard_ranges(const float* __restrict__ wtab, int L, int rows,
                                int64_t sec_lo, int64_t sec_hi, int64_t* __restrict__ lo,
                                int64_t* __restrict__ hi, int* __restrict__ mode,
                                float* __restrict__ cover) {
-  const int j = threadIdx.x;
-  if (j >= L) return;
-  // row of the smallest query radius present (rounded down)
+  // row of the smallest query radius present (rounded down); the widest
+  // window of each band over rows s0.. (blockDim = 32 x groups of rows)
+  __shared__ float part[32][33];
+  const int j = threadIdx.x & 31, g = threadIdx.x >> 5, ng = blockDim.x >> 5;
   const double pmin = __longlong_as_double((long long)*pmin_bits);
   const double rmin = fmax(0.0, 2.0 * atanh(pmin) * (1.0 - 1e-12) - 1e-9);
   const int s0 = (int)floor(rmin / (double)kRowStep);
+  float dm = -1.0f;
+  if (j < L)
+    for (int s = max(s0, 0) + g; s < rows; s += ng) dm = fmaxf(dm, wtab[s * L + j]);
+  part[g][j] = dm;
+  __syncthreads();
+  if (g != 0 || j >= L) return;
   float d = -1.0f;
-  for (int s = max(s0, 0); s < rows; ++s) d = fmaxf(d, wtab[s * L + j]);
+  for (int k = 0; k < ng; ++k) d = fmaxf(d, part[k][j]);
   const int64_t span = (int64_t)1 << 27;
   cover[j] = 1.0f;
   if (d < 0.0f) { mode[j] = -1; return; }
