@@ -100,6 +100,8 @@ struct hrg_context {
   int32_t* idx_final = nullptr;
   cudaEvent_t ev[9] = {};  // see enum Ev
   int query_blocks_per_sm = 0;
+  cudaStream_t aux[2] = {nullptr, nullptr};  // side streams of the row sorts
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
   unsigned char* h_rb = nullptr;  // mapped pinned readback area (kReadback bytes)
   unsigned char* d_rb = nullptr;  // its device alias
   int grid_light = 0, grid_light_wide = 0, grid_light_shard = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
@@ -450,6 +452,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     G.cbase = G.nb + 2 * gcap;
     G.chunk_row = c->chunk_row.as<int32_t>();
     G.cur = c->sub_cur.as<unsigned long long>();
+    J.giant = G.rows;
     CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
     if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
     else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
@@ -467,18 +470,29 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       CUDA_TRY(c->idx2.ensure(4 * (size_t)cap));
       const RowList none{nullptr, nullptr, nullptr};
       const unsigned sm = (unsigned)c->sm_count;
+      // the length classes are independent (rows were queued straight into
+      // their class): warp rows on the context's stream, block rows and the
+      // giant split on two side streams, joined before the readback
+      cudaStream_t s1 = c->aux[0], s2 = c->aux[1];
+      CUDA_TRY(cudaEventRecord(c->fork, st));
+      CUDA_TRY(cudaStreamWaitEvent(s1, c->fork, 0));
+      CUDA_TRY(cudaStreamWaitEvent(s2, c->fork, 0));
       k_sort_warp<<<HRG_SORT_GRID * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
       k_sort_rows<256, kBucketMax, kMidShift>
-          <<<HRG_SORT_GRID * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), st>>>(idx, idx, J.mid,
+          <<<HRG_SORT_GRID * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), s1>>>(idx, idx, J.mid,
                                                                                 J.large);
-      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
           idx, idx, J.large, G.rows);
-      k_giant_plan<<<1, 1024, 0, st>>>(G);
-      k_giant_hist<<<2 * sm, 1024, 0, st>>>(idx, G, n);
-      k_giant_scan<<<sm, 1024, 0, st>>>(G);
-      k_giant_scatter<<<2 * sm, 1024, 0, st>>>(idx, c->idx2.as<int32_t>(), G, n);
-      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), st>>>(
+      k_giant_plan<<<1, 1024, 0, s2>>>(G);
+      k_giant_hist<<<2 * sm, 1024, 0, s2>>>(idx, G, n);
+      k_giant_scan<<<sm, 1024, 0, s2>>>(G);
+      k_giant_scatter<<<2 * sm, 1024, 0, s2>>>(idx, c->idx2.as<int32_t>(), G, n);
+      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
           c->idx2.as<int32_t>(), idx, G.sub, none);
+      CUDA_TRY(cudaEventRecord(c->join[0], s1));
+      CUDA_TRY(cudaEventRecord(c->join[1], s2));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->join[0], 0));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->join[1], 0));
     }
     CUDA_TRY(cudaEventRecord(c->ev[E_ROWSORTED], st));
     CUDA_TRY(cudaGetLastError());
@@ -755,6 +769,15 @@ hrg_status hrg_context_create(int device, void* cuda_stream, hrg_context** out) 
       r = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_rb), c->h_rb, 0);
     if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
   }
+  {
+    cudaError_t r = cudaSuccess;
+    for (auto& a : c->aux)
+      if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
+    if (r == cudaSuccess) r = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+    for (auto& e : c->join)
+      if (r == cudaSuccess) r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
+  }
   // the sin/cos table of the fast path (device-global, idempotent)
   k_sincos_table<<<1, 256, 0, c->stream>>>();
   cudaError_t r = cudaStreamSynchronize(c->stream);
@@ -780,6 +803,11 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->widen})
     b->release();
   if (c->h_rb) cudaFreeHost(c->h_rb);
+  for (auto a : c->aux)
+    if (a) cudaStreamDestroy(a);
+  if (c->fork) cudaEventDestroy(c->fork);
+  for (auto e : c->join)
+    if (e) cudaEventDestroy(e);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   delete c;
   return HRG_OK;

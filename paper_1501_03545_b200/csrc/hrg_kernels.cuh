@@ -1672,10 +1672,17 @@ __device__ __forceinline__ void push_row(const RowList& R, int64_t off, int32_t 
 // Rows queued for an in-place sort of idx[dst, dst + len): every row is
 // contiguous by then (k_light compacts light rows, heavy rows are compacted
 // chunk by chunk), so a job is just its range.
+constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
+constexpr int kBucketMax = 4096;       // rows a 256-thread block sorts
+constexpr int kLargeMax = 24576;       // rows a 1024-thread block sorts (in + out: 221 KB)
+
+// Rows are queued by length straight into the list of the kernel that sorts
+// them, so the sort kernels are independent (they run on separate streams).
 struct SortJobs {
   RowList rows;    // queued rows, for k_sort_warp
   RowList mid;     // rows above kWarpBucketMax: k_sort_rows<256, kBucketMax>
   RowList large;   // rows above kBucketMax: k_sort_rows<1024, kLargeMax>
+  RowList giant;   // rows above kLargeMax: split by value first (k_giant_*)
 };
 
 // Queue a row; called by every lane of a warp (want = this lane has a row),
@@ -1684,6 +1691,9 @@ __device__ __forceinline__ void push_job_warp(const SortJobs& J, bool want, int6
                                               int32_t len) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const bool big = want && len > kWarpBucketMax;  // rare: one atomic each
+  if (big) push_row(len <= kBucketMax ? J.mid : (len <= kLargeMax ? J.large : J.giant), dst, len);
+  want = want && !big;
   const unsigned bal = __ballot_sync(FULL, want);
   if (!bal) return;
   unsigned base = 0;
@@ -1988,7 +1998,6 @@ __device__ bool group_bucket_sort(const int32_t* in, int32_t* tmp, int32_t* cnt,
   return true;
 }
 
-constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
 constexpr int kSortWarpThreads = 256;
 struct SortWarpSmem {
   int32_t in[kWarpBucketMax], tmp[kWarpBucketMax], cnt[32];
@@ -2082,9 +2091,7 @@ __global__ void __launch_bounds__(kSortWarpThreads, HRG_SORTWARP_MINB) k_sort_wa
   }
 }
 
-constexpr int kBucketMax = 4096;   // rows a 256-thread block sorts
 constexpr int kMidShift = HRG_MID_SHIFT;  // < 0: one bucket per thread, register networks
-constexpr int kLargeMax = 24576;   // rows a 1024-thread block sorts (in + out: 221 KB)
 template <int kCap, int kShift>
 constexpr size_t sort_rows_smem() {
   return sizeof(int32_t) * (2 * kCap + (kShift < 0 ? 1024 : (kCap >> kShift) + 1));
