@@ -82,7 +82,7 @@ struct hrg_context {
       sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_dst, job_len, mid_off, mid_len;
   int64_t stage_cap = 0;
   // index
-  Buf bands, dir, dir_total, bad, dir_gaps;
+  Buf bands, dir, dir_total, bad, dir_gaps, band_pmin;
   // CSR
   Buf deg, rowptr, idx, idx2, cand;
   Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep, sh_gid;
@@ -205,16 +205,20 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   QRec q{c->s_phi.as<double>(), c->s_rf.as<float>()};
   const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
                   c->vals_out.as<int32_t>()};
+  CUDA_TRY(c->band_pmin.ensure(8 * kMaxBands));
+  unsigned long long* band_pmin = c->band_pmin.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(band_pmin, 0xff, 8 * kMaxBands, st));
   if (sample_ids)
     k_gather<true><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
-        c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
-        nullptr, c->sh_sampled ? c->sh_gid.as<int32_t>() : nullptr, c->vals_out.as<int32_t>());
+        c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, nullptr,
+        nullptr, c->sh_sampled ? c->sh_gid.as<int32_t>() : nullptr, c->vals_out.as<int32_t>(),
+        band_pmin);
   else
     k_gather<false><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
         c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
-        c->s_rn.as<double>(), nullptr, nullptr);
+        c->s_rn.as<double>(), nullptr, nullptr, band_pmin);
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     // sector bounds on the sort granularity (multiples of 2^kSortShift)
@@ -227,9 +231,8 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
     qhi <<= kSortShift;
   }
   k_band_setup<<<1, 1024, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
-                                 c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr);
-  k_band_minmax<<<(unsigned)std::min<int64_t>(blocks_for(n), 8 * c->sm_count), 256, 0, st>>>(
-      n, c->keys_out.as<uint64_t>(), c->s_rp.as<double>(), c->bands.as<Band>());
+                                 c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr,
+                                 band_pmin);
   CUDA_TRY(c->dir_gaps.ensure(sizeof(DirGap) * (size_t)(n / 16 + 2 * kMaxBands + 8)));
   unsigned* ngaps = reinterpret_cast<unsigned*>(c->dir_total.as<char>() + 8);
   CUDA_TRY(cudaMemsetAsync(ngaps, 0, 4, st));
@@ -798,7 +801,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
-                 &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps,
+                 &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps, &c->band_pmin,
                  &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})
     b->release();

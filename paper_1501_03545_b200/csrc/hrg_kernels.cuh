@@ -1,23 +1,31 @@
 // hrg_kernels.cuh -- sm_100a kernels of the random-hyperbolic-graph generator.
 //
-// Pipeline (one CUDA stream, see hrg_api.cu):
-//   k_sample        Philox4x32-10 -> (phi, r_native, r_poincare) per vertex, plus a
-//                   59-bit sort key (radial band << 53 | angular fixed point q).
-//   cub radix sort  keys -> permutation into (band, angle) order.
-//   k_gather        48-byte fp64 candidate records in sorted order: p_x, p_y (the
-//                   point), c_x, c_y, rad^2 (its query circle), id; correctly
-//                   rounded sin/cos, hrgen's circle transform (geometry.py:141-157).
-//   k_band_setup / k_band_minmax / k_dir_fill / k_dir_tail
-//                   per band: position range, min hyperbolic radius, max Poincare
-//                   radius, and an angular directory (bucket -> first position).
-//   k_plan          per query: angular window of every band -> candidate count;
-//                   queries above kLightMax candidates are split into kChunk chunks.
-//   k_light<COUNT>  one thread per light query: bands in order, candidates in
-//                   position order, reference predicate, count hits.
-//   k_heavy<COUNT>  one warp per heavy chunk (hubs): lane j owns band j's window,
-//                   the warp walks the flattened segments 32 candidates at a time.
-//   cub scan        degrees -> CSR row pointers (+ per-chunk offsets of hubs).
-//   k_light/k_heavy<WRITE>  same traversals, writing the rows in order.
+// Pipeline (the context's stream; the row-sort classes on two side streams;
+// see hrg_api.cu and DESIGN.md):
+//   k_sample         Philox4x32-10 -> packed (phi, r_p), 32-bit sort key
+//                    (radial band << 27 | top 27 bits of the angle), id.
+//                    Sharded runs: k_shard_keys / k_shard_select /
+//                    k_shard_points keep only the points the sector can reach.
+//   cub radix sort   keys -> permutation into (band, angle) order.
+//   k_gather         48-byte fp64 candidate records in sorted order: p_x, p_y
+//                    (the point), c_x, c_y, rad^2 (its query circle), id;
+//                    correctly rounded sin/cos, hrgen's circle transform
+//                    (geometry.py:141-157); per-band innermost radius.
+//   k_band_setup / k_dir_fill / k_dir_gaps / k_dir_tail / k_window_table /
+//   k_tile_keys      per band: position and sector ranges, an angular
+//                    directory (bucket -> first position); per query-radius row
+//                    and band: the angular half-width of a conservative window;
+//                    query tiles (32 consecutive positions of one band).
+//   k_light          a warp per tile: per-band windows (shared by the tile where
+//                    the union is tiny), segments flattened, a lane-strided walk
+//                    over the candidates with the reference predicate, hits
+//                    compacted into staging; queries with too many candidates or
+//                    segments are deferred.
+//   k_heavy          a warp per 2048-candidate chunk of a deferred query (hubs).
+//   cub scan         degrees -> CSR row pointers (+ per-chunk offsets of hubs).
+//   k_compact_light / k_compact_heavy   staging -> CSR rows; rows of <= 64 ids
+//                    sorted in registers on the way.
+//   k_sort_warp / k_sort_rows / k_giant_*   longer rows sorted by length class.
 //
 // Replaces hrgen quadtree.py (build 303-340, pack 399-495, query_many 499-631)
 // and generator.py:190-225.
@@ -289,9 +297,34 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
                                                 double* __restrict__ s_rp,
                                                 double* __restrict__ s_rn,
                                                 const int32_t* __restrict__ gid,
-                                                int32_t* ids_out) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
+                                                int32_t* ids_out,
+                                                unsigned long long* __restrict__ band_pmin) {
+  // innermost Poincare radius per band (non-negative doubles order like
+  // their bits): warp reduction when a warp's points share a band (sorted
+  // positions: nearly always), shared memory, one global atomic per band
+  // per block
+  __shared__ unsigned long long s_pmin[kMaxBands];
+  if (threadIdx.x < kMaxBands) s_pmin[threadIdx.x] = ~0ull;
+  __syncthreads();
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = p < n;
+  {
+    const int band = ok ? (int)(k32[p] >> 27) : -1;
+    unsigned long long v = ok ? (unsigned long long)__double_as_longlong(pr[perm[p]].y) : ~0ull;
+    const unsigned FULL = 0xffffffffu;
+    const int b0 = __shfl_sync(FULL, band, 0);
+    if (__all_sync(FULL, band == b0)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+      if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicMin(&s_pmin[b0], v);
+    } else if (ok) {
+      atomicMin(&s_pmin[band], v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxBands && s_pmin[threadIdx.x] != ~0ull)
+    atomicMin(band_pmin + threadIdx.x, s_pmin[threadIdx.x]);
+  if (!ok) return;
   const int32_t i = perm[p];
   // sharded sampling: perm holds compact indices; ids_out (== perm) gets
   // the global vertex id in place (same element, same thread)
@@ -363,7 +396,8 @@ __device__ __forceinline__ int64_t warp_lower_bound_u64(const uint64_t* a, int64
 __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L,
                              uint64_t qsec_lo, uint64_t qsec_hi, Band* __restrict__ bands,
                              int64_t* __restrict__ dir_total,
-                             const float* __restrict__ cover) {
+                             const float* __restrict__ cover,
+                             const unsigned long long* __restrict__ band_pmin) {
   // searches by warp (block of 32 warps): band starts, then sector bounds
   __shared__ int64_t st[kMaxBands + 1], sq0[kMaxBands], sq1[kMaxBands];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -400,7 +434,9 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
     B.nb = 1 << lg;
     B.shift = kQBits - lg;
 
-    B.pmin = __longlong_as_double(0x7ff0000000000000ll);  // +inf until k_band_minmax
+    // innermost radius from k_gather (+inf for an empty band)
+    B.pmin = B.end > B.start ? __longlong_as_double((long long)band_pmin[j])
+                             : __longlong_as_double(0x7ff0000000000000ll);
     B.dir_base = 0;
     bands[j] = B;
   }
@@ -412,35 +448,6 @@ __global__ void k_band_setup(const uint64_t* __restrict__ keys, int64_t n, int L
   }
 }
 
-// Innermost Poincare radius of each band's points.  Sorted positions: a
-// warp's 32 points are nearly always one band, reduced in registers.
-__global__ void __launch_bounds__(256) k_band_minmax(int64_t n, const uint64_t* __restrict__ keys,
-                                                     const double* __restrict__ s_rp,
-                                                     Band* __restrict__ bands) {
-  __shared__ unsigned long long sp[kMaxBands];
-  if (threadIdx.x < kMaxBands) sp[threadIdx.x] = 0x7ff0000000000000ull;
-  __syncthreads();
-  const unsigned FULL = 0xffffffffu;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x; p0 < n; p0 += stride) {
-    const int64_t p = p0 + threadIdx.x;
-    const bool ok = p < n;
-    const int band = ok ? (int)(keys[p] >> kQBits) : -1;
-    // non-negative doubles order like their bit patterns
-    unsigned long long v = ok ? (unsigned long long)__double_as_longlong(s_rp[p]) : ~0ull;
-    const int b0 = __shfl_sync(FULL, band, 0);
-    if (__all_sync(FULL, band == b0)) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
-      if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicMin(&sp[b0], v);
-    } else if (ok) {
-      atomicMin(&sp[band], v);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < kMaxBands && sp[threadIdx.x] != 0x7ff0000000000000ull)
-    atomicMin(reinterpret_cast<unsigned long long*>(&bands[threadIdx.x].pmin), sp[threadIdx.x]);
-}
 
 // dir[base + k] = first position of the band whose bucket >= k.
 // dir[b] = first position of the band whose bucket is >= b: every point

@@ -344,6 +344,35 @@ def test_out_of_bounds_coordinates_raise():
         P.generate(GeneratorParams(n=10, radius=80.0, alpha=1.0))
 
 
+def test_two_contexts_concurrently():
+    """Two generator contexts on their own streams, driven from two host
+    threads at once (bench.py's e2e pattern), each reproduce the graph."""
+    import threading
+    import torch
+    p = GeneratorParams(n=200_000, avg_degree=24.0, gamma=2.4, seed=11)
+    ref = P.generate(p)
+    model = p.resolve()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    engines = [P.Engine(0, stream=s.cuda_stream) for s in streams]
+    out = {}
+
+    def run(w):
+        res = []
+        for _ in range(3):
+            engines[w].generate(model, p.seed)
+            res.append(engines[w].copy_csr(np.int64))
+        out[w] = res
+
+    ths = [threading.Thread(target=run, args=(w,)) for w in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for w in range(2):
+        for ip, ix in out[w]:
+            assert np.array_equal(ip, ref.indptr) and np.array_equal(ix, ref.indices)
+
+
 def test_device_csr_tensors():
     import torch
     eng = P.get_engine()
