@@ -73,6 +73,9 @@ namespace hrg {
 #ifndef HRG_SEGCAP
 #define HRG_SEGCAP 28
 #endif
+#ifndef HRG_LIGHT_MAX
+#define HRG_LIGHT_MAX 2048
+#endif
 #ifndef HRG_TILE_HITS
 #define HRG_TILE_HITS 2048
 #endif
@@ -534,7 +537,7 @@ __global__ void k_dir_tail(const uint64_t* __restrict__ keys, const Band* __rest
              threadIdx.x, blockDim.x);
 }
 
-constexpr int kLightMax = 2048;    // queries with more candidates take the heavy path
+constexpr int kLightMax = HRG_LIGHT_MAX;  // queries with more candidates take the heavy path
 constexpr int kSegCap = HRG_SEGCAP;  // non-empty band segments a light query may hold
 constexpr int kChunk = 2048;       // heavy-path work item: candidates of one query
 constexpr int kLightThreads = 128;
