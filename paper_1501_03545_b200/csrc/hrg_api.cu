@@ -84,7 +84,9 @@ struct hrg_context {
   // index
   Buf bands, dir, dir_total, bad, dir_gaps, band_pmin;
   // CSR
-  Buf deg, rowptr, idx, idx2, cand;
+  Buf deg, rowptr, idx, idx2, cand, rowidx, row_ids, rowptr_c, nq_buf;
+  bool compact_result = false;  // sharded: rows in sector-position order (expanded on request)
+  int64_t nq = 0;
   Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep, sh_gid;
   bool sh_sampled = false;  // sharded sampling: vals are compact indices, sh_gid the ids
   Buf widen;
@@ -164,20 +166,25 @@ inline unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)std::max<i
 // readback never queues behind another context's multi-GB result copy.
 constexpr size_t kReadback = 256;
 struct RbItem { const void* src; size_t bytes; };
-__global__ void k_readback(RbItem a, RbItem b, unsigned char* dst) {
+__global__ void k_readback(RbItem a, RbItem b, RbItem e, unsigned char* dst) {
   for (size_t i = threadIdx.x; i < a.bytes; i += blockDim.x)
     dst[i] = static_cast<const unsigned char*>(a.src)[i];
   for (size_t i = threadIdx.x; i < b.bytes; i += blockDim.x)
     dst[a.bytes + i] = static_cast<const unsigned char*>(b.src)[i];
+  for (size_t i = threadIdx.x; i < e.bytes; i += blockDim.x)
+    dst[a.bytes + b.bytes + i] = static_cast<const unsigned char*>(e.src)[i];
 }
 
 hrg_status readback(hrg_context* c, const void* src_a, size_t na, void* dst_a,
-                    const void* src_b = nullptr, size_t nb = 0, void* dst_b = nullptr) {
-  k_readback<<<1, 128, 0, c->stream>>>(RbItem{src_a, na}, RbItem{src_b, nb}, c->d_rb);
+                    const void* src_b = nullptr, size_t nb = 0, void* dst_b = nullptr,
+                    const void* src_e = nullptr, size_t ne = 0, void* dst_e = nullptr) {
+  k_readback<<<1, 128, 0, c->stream>>>(RbItem{src_a, na}, RbItem{src_b, nb}, RbItem{src_e, ne},
+                                       c->d_rb);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   memcpy(dst_a, c->h_rb, na);
   if (nb) memcpy(dst_b, c->h_rb + na, nb);
+  if (ne) memcpy(dst_e, c->h_rb + na + nb, ne);
   return HRG_OK;
 }
 
@@ -273,7 +280,7 @@ hrg_status scan_i32_to_i64(hrg_context* c, const int32_t* in, int64_t* out, int6
 // Light query pass, heavy (hub) pass, scans, compaction (+ row sort when ids
 // are not positions).
 hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool sample_ids,
-                      hrg_stats* stats) {
+                      bool compact, hrg_stats* stats) {
   const int64_t n = M->n;   // vertex ids (rows)
   const int64_t np = c->np; // indexed positions
   cudaStream_t st = c->stream;
@@ -298,6 +305,23 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   A.heavy_c = c->heavy_c.as<int32_t>();
   A.heavy_of = c->heavy_of.as<int32_t>();
   A.deg = c->deg.as<int32_t>();
+  A.rowidx = nullptr;
+  // sharded runs: compact rows, one per query of the sector in position
+  // order (the n-row CSR of the API is assembled on request); the row
+  // count is bounded by the indexed points
+  const int64_t nrows = compact ? np : n;
+  int64_t* rowbuf = c->rowptr.as<int64_t>();
+  if (compact) {
+    CUDA_TRY(c->rowidx.ensure(4 * (size_t)np));
+    CUDA_TRY(c->row_ids.ensure(4 * (size_t)np));
+    CUDA_TRY(c->rowptr_c.ensure(8 * (size_t)(np + 1)));
+    CUDA_TRY(c->nq_buf.ensure(8));
+    k_rowidx<<<4 * c->sm_count, 256, 0, st>>>(A.bands, L, c->vals_out.as<int32_t>(),
+                                              c->rowidx.as<int32_t>(), c->row_ids.as<int32_t>(),
+                                              c->nq_buf.as<int64_t>());
+    A.rowidx = c->rowidx.as<int32_t>();
+    rowbuf = c->rowptr_c.as<int64_t>();
+  }
 
   // window table: one row per 1/16 of query radius, one column per band.
   // 2^-45 bounds the absolute fp64 error of dx*dx+dy*dy and rad^2 (all
@@ -394,7 +418,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     A.chunk_hits = c->chunk_hits.as<int32_t>();
     A.total_chunks = d_chunks;
 
-    CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
+    CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * nrows, st));
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
     {
@@ -415,11 +439,11 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     else k_heavy<false><<<c->grid_heavy, 256, 0, st>>>(A, 0);
     CUDA_TRY(cudaEventRecord(c->ev[E_COUNTED], st));
     CUDA_TRY(cudaGetLastError());
-    hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
+    hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), rowbuf, nrows);
     if (s != HRG_OK) return s;
 
     int32_t* idx = c->idx.as<int32_t>();
-    const int64_t* rp = c->rowptr.as<int64_t>();
+    const int64_t* rp = rowbuf;
     // sort jobs (sample order): light rows above kSmallSlots ids, heavy rows
     const int64_t jcap = 2 * np + 1;
     const int64_t mcap = cap / (kWarpBucketMax + 1) + 1;
@@ -501,7 +525,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaGetLastError());
     // the one synchronisation: counters, edge total, overflow flag
     {
-      hrg_status rs = readback(c, c->counters.p, 128, ctr, c->rowptr.as<int64_t>() + n, 8, &nnz);
+      hrg_status rs = readback(c, c->counters.p, 128, ctr, rowbuf + nrows, 8, &nnz,
+                               compact ? c->nq_buf.p : nullptr, compact ? 8 : 0, &c->nq);
       if (rs != HRG_OK) return rs;
     }
     total_chunks = (int64_t)ctr[14];
@@ -514,6 +539,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   c->stage_cap = std::max<int64_t>(c->stage_cap, (int64_t)(ctr[0] + ctr[0] / 10 + 4096));
   launches += 9 + (sample_ids ? 9 : 0);  // light, heavy prep+pass, 3 scans, compaction(s), sorts
   c->nnz = nnz;
+  c->compact_result = compact;
   if (stats) {
     stats->nnz = nnz;
     stats->m = nnz / 2;
@@ -728,7 +754,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   s = build_index(c, M, S, L, shard, C, sample_ids);
   if (s != HRG_OK) return s;
   if (stats) stats->kernel_launches = 7;  // sample/keys, gather, 5 index kernels (+ CUB sort)
-  s = emit_edges(c, M, L, C, sample_ids, stats);
+  s = emit_edges(c, M, L, C, sample_ids, shard && shard->count > 1 && sample_ids, stats);
   if (s != HRG_OK) return s;
   CUDA_TRY(cudaStreamSynchronize(st));
   c->n = n;
@@ -744,6 +770,29 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     stats->t_compact_ms = ev_ms(c->ev[E_WRITE0], c->ev[E_WRITTEN]);
     stats->t_rowsort_ms = ev_ms(c->ev[E_WRITTEN], c->ev[E_ROWSORTED]);
   }
+  return HRG_OK;
+}
+
+// Sharded result: compact rows -> the n-row CSR of the API, once, on request.
+hrg_status expand_rows(hrg_context* c) {
+  if (!c->compact_result) return HRG_OK;
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
+  k_expand_deg<<<4 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
+                                                c->row_ids.as<int32_t>(), c->deg.as<int32_t>());
+  hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
+  if (s != HRG_OK) return s;
+  // the compact rows are in idx (the compaction's output); idx2 is scratch
+  // once the row sorts are done
+  CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(c->nnz, 1)));
+  int32_t* out = c->idx2.as<int32_t>();
+  k_expand_rows<<<8 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
+                                                 c->row_ids.as<int32_t>(), c->idx_final,
+                                                 c->rowptr.as<int64_t>(), out);
+  CUDA_TRY(cudaGetLastError());
+  c->idx_final = out;
+  c->compact_result = false;
   return HRG_OK;
 }
 
@@ -802,7 +851,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps, &c->band_pmin,
-                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
+                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->rowidx, &c->row_ids, &c->rowptr_c, &c->nq_buf, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})
     b->release();
   if (c->h_rb) cudaFreeHost(c->h_rb);
@@ -967,6 +1016,11 @@ hrg_status hrg_result_device_ptrs(hrg_context* c, const double** phi, const doub
     CUDA_TRY(cudaGetLastError());
     c->coords_pending = false;
   }
+  if (indptr || indices) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    hrg_status es = expand_rows(c);
+    if (es != HRG_OK) return es;
+  }
   if (phi) *phi = c->coords_sorted ? c->s_phi.as<double>() : c->phi.as<double>();
   if (rn) *rn = c->coords_sorted ? c->s_rn.as<double>() : c->rn.as<double>();
   if (rp) *rp = c->coords_sorted ? c->s_rp.as<double>() : c->rp.as<double>();
@@ -985,6 +1039,10 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
   cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   size_t d = sizeof(double) * (size_t)c->n;
   const double *sp = nullptr, *sn = nullptr, *sr = nullptr;
+  if (indptr || indices) {
+    hrg_status es = expand_rows(c);
+    if (es != HRG_OK) return es;
+  }
   hrg_status s = hrg_result_device_ptrs(c, phi ? &sp : nullptr, rn ? &sn : nullptr,
                                         rp ? &sr : nullptr, nullptr, nullptr);
   if (s != HRG_OK) return s;

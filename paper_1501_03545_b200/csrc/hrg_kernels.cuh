@@ -570,7 +570,11 @@ struct QueryArgs {
   const int32_t* chunk_entry;// chunk -> entry
   const int64_t* total_chunks;  // device scalar (k_heavy_prep)
   int32_t* chunk_hits;
-  int32_t* deg;              // row length per vertex id
+  int32_t* deg;              // row length per output row
+  // output row of a sorted position: nullptr = the vertex id (ids[] in
+  // sample order, the position itself in angular order); sharded runs:
+  // compact rows, one per query of the sector, in position order
+  const int32_t* rowidx;
   unsigned long long* cand_total;
   // query tiles: 32 consecutive positions of one band (start | end << 32;
   // ~0 = no tile)
@@ -578,6 +582,36 @@ struct QueryArgs {
   int64_t ntiles;            // entries (an upper bound on the tiles)
   unsigned long long* tile_next;  // dynamic tile counters: k_light, k_compact_light
 };
+
+template <bool kSampleIds>
+__device__ __forceinline__ int32_t row_of(const QueryArgs& A, int32_t v) {
+  return A.rowidx ? __ldg(A.rowidx + v) : (kSampleIds ? __ldg(A.rec.ids + v) : v);
+}
+
+// Compact rows of a sharded run: row k = the k-th query position of the
+// sector (bands in order), rowidx[pos] = k, row_ids[k] = its vertex id;
+// nq = the row count.
+__global__ void k_rowidx(const Band* __restrict__ bands, int L, const int32_t* __restrict__ ids,
+                         int32_t* __restrict__ rowidx, int32_t* __restrict__ row_ids,
+                         int64_t* __restrict__ nq) {
+  __shared__ int64_t base[kMaxBands + 1];
+  if (threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int j = 0; j < L; ++j) { base[j] = a; a += max(0, bands[j].qend - bands[j].qstart); }
+    base[L] = a;
+    if (blockIdx.x == 0) *nq = a;
+  }
+  __syncthreads();
+  const int64_t total = base[L];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (j + 1 < L && base[j + 1] <= k) ++j;
+    const int32_t pos = bands[j].qstart + (int32_t)(k - base[j]);
+    rowidx[pos] = (int32_t)k;
+    row_ids[k] = ids[pos];
+  }
+}
 
 // Tile table: every band's query range cut into tiles of 32 positions (the
 // key is the angular key of the tile's first point, for an angular
@@ -1378,7 +1412,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
       }
     }
     __syncwarp();
-    if (light) A.deg[kSampleIds ? __ldg(A.rec.ids + v) : v] = fits ? sm.hits[tid] : 0;
+    if (light) A.deg[row_of<kSampleIds>(A, v)] = fits ? sm.hits[tid] : 0;
     __syncwarp();
   }
 #pragma unroll
@@ -1533,7 +1567,7 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
     if (lane == 0) {
       if (!fits) atomicOr(A.overflow, 1);
       A.chunk_hits[c] = hits;
-      atomicAdd(&A.deg[f.idv], hits);
+      atomicAdd(&A.deg[row_of<kSampleIds>(A, v)], hits);
     }
   }
 }
@@ -1765,7 +1799,7 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
     // independent loads first (one round trip), then the row's CSR offset;
     // a light row's length is its hit count k_light left in slots[]
     const int32_t hv = active ? A.heavy_of[v] : 0;
-    const int32_t idv = active ? (kSampleIds ? __ldg(A.rec.ids + v) : v) : 0;
+    const int32_t idv = active ? row_of<kSampleIds>(A, v) : 0;
     const int32_t sl = active ? A.slots[v] : 0;
     const int64_t so = active ? A.stage_off[v] : INT64_MAX;
     const bool light = active && hv < 0;
@@ -2403,7 +2437,7 @@ __global__ void __launch_bounds__(256) k_compact_heavy(QueryArgs A, int64_t H,
   for (int64_t c = warp; c < total_chunks; c += nwarps) {
     const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
-    const int32_t idv = sample_ids ? __ldg(A.rec.ids + v) : v;
+    const int32_t idv = sample_ids ? row_of<true>(A, v) : row_of<false>(A, v);
     const int64_t c0 = A.chunk_start[e];
     const int64_t d = rowptr[idv] + (chunk_off[c] - chunk_off[c0]);
     const int32_t h = A.chunk_hits[c];
@@ -2436,7 +2470,7 @@ __global__ void k_queue_heavy_rows(QueryArgs A, const int64_t* __restrict__ rowp
     int64_t b = 0;
     int32_t len = 0;
     if (e < H) {
-      const int32_t idv = __ldg(A.rec.ids + A.heavy_v[e]);
+      const int32_t idv = row_of<true>(A, A.heavy_v[e]);
       b = rowptr[idv];
       len = (int32_t)(rowptr[idv + 1] - b);
     }
@@ -2477,6 +2511,30 @@ __global__ void __launch_bounds__(256) k_sincos_compare(int64_t n, uint64_t seed
   }
   atomicAdd(out, bad);
   atomicAdd(out + 1, slow);
+}
+
+// Compact rows -> the n-row CSR of the API (on request): degrees by vertex
+// id, then every row copied to its place, a warp per row.
+__global__ void __launch_bounds__(256) k_expand_deg(int64_t nq, const int64_t* __restrict__ rp_c,
+                                                    const int32_t* __restrict__ row_ids,
+                                                    int32_t* __restrict__ deg) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nq;
+       k += (int64_t)gridDim.x * blockDim.x)
+    deg[row_ids[k]] = (int32_t)(rp_c[k + 1] - rp_c[k]);
+}
+
+__global__ void __launch_bounds__(256) k_expand_rows(int64_t nq, const int64_t* __restrict__ rp_c,
+                                                     const int32_t* __restrict__ row_ids,
+                                                     const int32_t* __restrict__ idx_c,
+                                                     const int64_t* __restrict__ rp,
+                                                     int32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = w0; k < nq; k += nw) {
+    const int64_t s = rp_c[k], len = rp_c[k + 1] - s, d = rp[row_ids[k]];
+    for (int64_t i = lane; i < len; i += 32) idx[d + i] = idx_c[s + i];
+  }
 }
 
 __global__ void __launch_bounds__(256) k_widen(int64_t n, const int32_t* __restrict__ in,
