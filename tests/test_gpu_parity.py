@@ -264,6 +264,24 @@ def test_shards_union_is_the_graph(kw, count):
     assert np.array_equal(acc, np.diff(full.indptr))
 
 
+def test_shards_from_coordinates(oracle):
+    """Sharded runs on caller-given coordinates (hrgen's own, R = 33.2) give
+    the reference rows; their union is the reference graph."""
+    run = max([r for r in RUNS if r.n >= 10_000], key=lambda r: r.R)
+    coords = VertexCoordinates(phi=run.phi, r_native=None, r_poincare=run.r_poincare)
+    full = P.edges_from_coordinates(coords, run.R, alpha=run.alpha)
+    assert edge_set_hash(oracle, full) == run.edge_sha256
+    acc = np.zeros(full.n, np.int64)
+    for k in range(5):
+        g = P.edges_from_coordinates(coords, run.R, alpha=run.alpha, shard=P.Shard(k, 5))
+        deg = np.diff(g.indptr)
+        assert np.all(acc[deg > 0] == 0)
+        acc += deg
+        for v in np.flatnonzero(deg)[:500]:
+            assert np.array_equal(g.neighbors(v), full.neighbors(v))
+    assert np.array_equal(acc, np.diff(full.indptr))
+
+
 # ------------------------------------------------------------ properties
 def test_full_size_config2_properties():
     """BASELINE config 2 (n=1e7, k=32, gamma=2.5, seed 2): hrgen Graph
