@@ -1787,24 +1787,36 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
   int32_t* sm = buf[threadIdx.x >> 5];
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // The per-row loads of a tile (its entry in the tile table, then heavy
+  // flag, row, hit count, staging offset, then the row's CSR offset) are
+  // dependent DRAM round trips; the next tile's are issued while this one is
+  // copied and sorted (software pipelining across the dynamic tile loop).
+  struct Pro { uint64_t tv; int32_t hv, idv, sl; int64_t so; };
+  auto fetch = [&](int64_t t) {
+    Pro P;
+    P.tv = t < A.ntiles ? __ldg(A.tiles + t) : ~0ull;
+    const int32_t v0 = (int32_t)(P.tv & 0xffffffffu) + lane;
+    const bool act = P.tv != ~0ull && v0 < (int32_t)(P.tv >> 32);
+    const int32_t vv = act ? v0 : 0;
+    P.hv = act ? A.heavy_of[vv] : 0;
+    P.idv = act ? row_of<kSampleIds>(A, vv) : 0;
+    P.sl = act ? A.slots[vv] : 0;
+    P.so = act ? A.stage_off[vv] : INT64_MAX;
+    return P;
+  };
   int64_t tk = wid;
-  for (; tk < A.ntiles;
-       tk = __shfl_sync(FULL, lane == 0 ? (int64_t)(nw + atomicAdd(A.tile_next + 1, 1ull)) : 0,
-                        0)) {
-    const uint64_t tv = __ldg(A.tiles + tk);
-    if (tv == ~0ull) break;
+  Pro cur = fetch(tk);
+  while (tk < A.ntiles && cur.tv != ~0ull) {
+    const int64_t tn =
+        __shfl_sync(FULL, lane == 0 ? (int64_t)(nw + atomicAdd(A.tile_next + 1, 1ull)) : 0, 0);
+    const uint64_t tv = cur.tv;
     const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
     const bool active = v0 < (int32_t)(tv >> 32);
-    const int32_t v = active ? v0 : 0;
-    // independent loads first (one round trip), then the row's CSR offset;
     // a light row's length is its hit count k_light left in slots[]
-    const int32_t hv = active ? A.heavy_of[v] : 0;
-    const int32_t idv = active ? row_of<kSampleIds>(A, v) : 0;
-    const int32_t sl = active ? A.slots[v] : 0;
-    const int64_t so = active ? A.stage_off[v] : INT64_MAX;
-    const bool light = active && hv < 0;
-    const int32_t ns = light ? sl : 0, len = ns;
-    const int64_t dst = light ? rowptr[idv] : 0, src = light ? so : INT64_MAX;
+    const bool light = active && cur.hv < 0;
+    const int32_t ns = light ? cur.sl : 0, len = ns;
+    const int64_t dst = light ? rowptr[cur.idv] : 0, src = light ? cur.so : INT64_MAX;
+    const Pro nxt = fetch(tn);
     int64_t base = src;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) base = min(base, (int64_t)__shfl_xor_sync(FULL, base, o));
@@ -1930,6 +1942,8 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
         l0 = l1;
       }
     }
+    tk = tn;
+    cur = nxt;
   }
 }
 
