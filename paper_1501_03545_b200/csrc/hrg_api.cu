@@ -8,7 +8,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
 #include <cmath>
@@ -268,7 +268,7 @@ hrg_status scan_i32_to_i64(hrg_context* c, const int32_t* in, int64_t* out, int6
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemsetAsync(out, 0, 8, st));
   if (n == 0) return HRG_OK;
-  cub::TransformInputIterator<long long, ToI64, const int32_t*> it(in, ToI64());
+  auto it = thrust::make_transform_iterator(in, ToI64());
   size_t tb = 0;
   CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, it, (long long*)out + 1, (int)n, st));
   CUDA_TRY(c->temp.ensure(tb));
