@@ -76,6 +76,9 @@ namespace hrg {
 #ifndef HRG_LIGHT_MAX
 #define HRG_LIGHT_MAX 2048
 #endif
+#ifndef HRG_WARP_BUCKET_MAX
+#define HRG_WARP_BUCKET_MAX 512
+#endif
 #ifndef HRG_TILE_HITS
 #define HRG_TILE_HITS 2048
 #endif
@@ -1716,7 +1719,7 @@ __device__ __forceinline__ void push_row(const RowList& R, int64_t off, int32_t 
 // Rows queued for an in-place sort of idx[dst, dst + len): every row is
 // contiguous by then (k_light compacts light rows, heavy rows are compacted
 // chunk by chunk), so a job is just its range.
-constexpr int kWarpBucketMax = 512;   // rows a warp sorts in shared memory
+constexpr int kWarpBucketMax = HRG_WARP_BUCKET_MAX;   // rows a warp sorts in shared memory
 constexpr int kBucketMax = 4096;       // rows a 256-thread block sorts
 constexpr int kLargeMax = 24576;       // rows a 1024-thread block sorts (in + out: 221 KB)
 
