@@ -19,8 +19,9 @@ pytestmark = pytest.mark.gpu
 
 SWEEP = [dict(n=10_000_000, avg_degree=k, gamma=g, seed=4)
          for k in (4.0, 64.0, 256.0) for g in (2.2, 3.0, 5.0)]
-CASES = ([dict(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2)] + SWEEP
-         + [dict(n=100_000_000, avg_degree=16.0, gamma=3.0, seed=3)])
+CASES = ([dict(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2),
+          dict(n=10_000_000, avg_degree=32.0, gamma=2.5, seed=2, vertex_order="angular")]
+         + SWEEP + [dict(n=100_000_000, avg_degree=16.0, gamma=3.0, seed=3)])
 CHUNK = 1 << 27
 
 
@@ -55,13 +56,13 @@ def device_invariants(ip, ix, n):
 
 
 @pytest.mark.parametrize("kw", CASES, ids=lambda k: f"n{k['n']:.0e}-k{k['avg_degree']:g}"
-                         f"-g{k['gamma']:g}-s{k['seed']}")
+                         f"-g{k['gamma']:g}-s{k['seed']}" + ("-angular" if "vertex_order" in k else ""))
 def test_full_size_rows_match_oracle(oracle, kw):
     import torch
     p = GeneratorParams(**kw)
     model = p.resolve()
     eng = P.get_engine()
-    st = eng.generate(model, p.seed)
+    st = eng.generate(model, p.seed, P.generator.VERTEX_ORDERS[p.vertex_order])
     ip, ix = eng.device_csr()
     n = model.n
     deg = device_invariants(ip, ix, n)
