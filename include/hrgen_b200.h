@@ -123,6 +123,17 @@ hrg_status hrg_edges_from_coords(hrg_context *ctx, const hrg_model *model, const
                                  const double *r_poincare, int mem_kind, const hrg_shard *shard,
                                  hrg_stats *stats);
 
+/* hrgen generator.py:249-274 generate_brute_force(coords, R) itself: all
+ * pairs, edge iff 2 asinh(sqrt(d2 / (b_i b_j))) < R with x = r cos(phi),
+ * y = r sin(phi), b = (1 - r)(1 + r), d2 = dx*dx + dy*dy (hrgen's sequence).
+ * O(n^2), for validation.  *near_ties (optional) receives the number of
+ * ordered pairs whose distance is within 4 ulps of R, where the device's asinh
+ * and libm's may round differently.  Ids = array index; result as for
+ * hrg_generate. */
+hrg_status hrg_edges_brute_force(hrg_context *ctx, int64_t n, const double *phi,
+                                 const double *r_poincare, int mem_kind, double R,
+                                 int64_t *near_ties);
+
 /* Sizes of the last result. */
 hrg_status hrg_result_sizes(hrg_context *ctx, int64_t *n, int64_t *nnz);
 

@@ -37,7 +37,7 @@ EXPORTED = (
     "hrg_context_set_stream", "hrg_expected_avg_degree", "hrg_target_radius", "hrg_model_init",
     "hrg_generate", "hrg_sample_points", "hrg_edges_from_coords", "hrg_result_sizes",
     "hrg_copy_result", "hrg_result_device_ptrs", "hrg_host_alloc", "hrg_host_free",
-    "hrg_synchronize", "hrg_debug_sincos", "hrg_debug_sincos_compare",
+    "hrg_synchronize", "hrg_debug_sincos", "hrg_debug_sincos_compare", "hrg_edges_brute_force",
 )
 
 
@@ -104,6 +104,8 @@ def _declare(L):
         "hrg_synchronize": (S, [_vp]),
         "hrg_debug_sincos": (S, [_vp, ctypes.c_int64, _vp, _vp, _vp]),
         "hrg_debug_sincos_compare": (S, [_vp, ctypes.c_int64, ctypes.c_uint64, _vp, _vp]),
+        "hrg_edges_brute_force": (S, [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int, ctypes.c_double,
+                                      _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

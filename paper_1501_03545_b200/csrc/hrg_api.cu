@@ -998,6 +998,60 @@ hrg_status hrg_edges_from_coords(hrg_context* c, const hrg_model* M, const doubl
   return run_pipeline(c, M, shard, true, true, 0, stats);
 }
 
+hrg_status hrg_edges_brute_force(hrg_context* c, int64_t n, const double* phi, const double* rp,
+                                 int mem_kind, double R, int64_t* near_ties) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  if (n < 1) return fail(HRG_ERR_PARAMETER_DOMAIN, "n must be at least 1");
+  if (n >= (int64_t)1 << 30) return fail(HRG_ERR_PARAMETER_DOMAIN, "n must be below 2^30");
+  if (!(R > 0.0)) return fail(HRG_ERR_PARAMETER_DOMAIN, "radius must be positive");
+  if (!phi || !rp) return fail(HRG_ERR_PARAMETER_DOMAIN, "coordinate pointer is NULL");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->have_result = false;
+  hrg_status s = ensure_point_buffers(c, n);
+  if (s != HRG_OK) return s;
+  cudaStream_t st = c->stream;
+  cudaMemcpyKind k = mem_kind == HRG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_TRY(cudaMemcpyAsync(c->phi.p, phi, sizeof(double) * n, k, st));
+  CUDA_TRY(cudaMemcpyAsync(c->rp.p, rp, sizeof(double) * n, k, st));
+  // x, y, b in the sorted-record buffers (free outside a generation)
+  double* x = c->s_phi.as<double>();
+  double* y = c->s_rn.as<double>();
+  double* b = c->s_rp.as<double>();
+  k_bf_points<<<blocks_for(n), 256, 0, st>>>(n, c->phi.as<double>(), c->rp.as<double>(), x, y, b);
+  const double S = std::sinh(R / 2.0);
+  const double t_lo = (S * (1.0 - 1e-9)) * (S * (1.0 - 1e-9));
+  const double t_hi = (S * (1.0 + 1e-9)) * (S * (1.0 + 1e-9));
+  const double tie = 4.0 * (std::nextafter(R, INFINITY) - R);
+  CUDA_TRY(c->cand.ensure(8));
+  unsigned long long* d_ties = c->cand.as<unsigned long long>();
+  CUDA_TRY(cudaMemsetAsync(d_ties, 0, 8, st));
+  k_bf_pairs<false><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie,
+                                                    c->deg.as<int32_t>(), nullptr, nullptr,
+                                                    nullptr);
+  s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
+  if (s != HRG_OK) return s;
+  int64_t nnz = 0;
+  s = readback(c, c->rowptr.as<int64_t>() + n, 8, &nnz);
+  if (s != HRG_OK) return s;
+  CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
+  k_bf_pairs<true><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie, nullptr,
+                                                   c->rowptr.as<int64_t>(), c->idx.as<int32_t>(),
+                                                   d_ties);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long ties = 0;
+  s = readback(c, d_ties, 8, &ties);
+  if (s != HRG_OK) return s;
+  if (near_ties) *near_ties = (int64_t)ties;
+  c->n = n;
+  c->nnz = nnz;
+  c->idx_final = c->idx.as<int32_t>();
+  c->compact_result = false;
+  c->coords_pending = false;
+  c->coords_sorted = false;
+  c->have_result = true;
+  return HRG_OK;
+}
+
 hrg_status hrg_result_sizes(hrg_context* c, int64_t* n, int64_t* nnz) {
   if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
   if (n) *n = c->n;

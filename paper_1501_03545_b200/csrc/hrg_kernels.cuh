@@ -2530,6 +2530,79 @@ __global__ void __launch_bounds__(256) k_sincos_compare(int64_t n, uint64_t seed
   atomicAdd(out + 1, slow);
 }
 
+// ---- all-pairs reference (hrgen generator.py:249-274, generate_brute_force):
+// x = r cos(phi), y = r sin(phi), b = (1 - r)(1 + r); {i, j} is an edge iff
+// 2 asinh(sqrt(d2 / (b_i b_j))) < R with d2 = dx*dx + dy*dy, evaluated in that
+// order.  The predicate is symmetric (fl(a - b) = -fl(b - a)), so every row
+// scans all columns in ascending order and comes out sorted.  A pair far from
+// the threshold is decided by d2 against (sinh(R/2)(1 -+ 1e-9))^2 b_i b_j
+// (no division, sqrt or asinh); the others by hrgen's own sequence, and those
+// within 4 ulps of R -- where CUDA's asinh and glibc's may round differently
+// -- are counted as near ties.
+__global__ void __launch_bounds__(256) k_bf_points(int64_t n, const double* __restrict__ phi,
+                                                   const double* __restrict__ rp,
+                                                   double* __restrict__ x, double* __restrict__ y,
+                                                   double* __restrict__ b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double sn, cs;
+  sincos_crf(phi[i], &sn, &cs);
+  const double r = rp[i];
+  x[i] = __dmul_rn(r, cs);
+  y[i] = __dmul_rn(r, sn);
+  b[i] = __dmul_rn(__dsub_rn(1.0, r), __dadd_rn(1.0, r));
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(256) k_bf_pairs(int64_t n, const double* __restrict__ x,
+                                                  const double* __restrict__ y,
+                                                  const double* __restrict__ b, double t_lo,
+                                                  double t_hi, double R, double tie,
+                                                  int32_t* __restrict__ deg,
+                                                  const int64_t* __restrict__ rowptr,
+                                                  int32_t* __restrict__ idx,
+                                                  unsigned long long* __restrict__ ties) {
+  __shared__ double sx[256], sy[256], sbb[256];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = i < n;
+  const double xi = ok ? x[i] : 0.0, yi = ok ? y[i] : 0.0, bi = ok ? b[i] : 0.0;
+  int32_t cnt = 0;
+  int64_t at = (kWrite && ok) ? rowptr[i] : 0;
+  unsigned long long nt = 0;
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    __syncthreads();
+    const int64_t jj = j0 + threadIdx.x;
+    sx[threadIdx.x] = jj < n ? x[jj] : 0.0;
+    sy[threadIdx.x] = jj < n ? y[jj] : 0.0;
+    sbb[threadIdx.x] = jj < n ? b[jj] : 0.0;
+    __syncthreads();
+    const int m = (int)min((int64_t)256, n - j0);
+    if (!ok) continue;
+    for (int t = 0; t < m; ++t) {
+      const int64_t j = j0 + t;
+      const double dx = __dsub_rn(xi, sx[t]), dy = __dsub_rn(yi, sy[t]);
+      const double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+      const double bb = __dmul_rn(bi, sbb[t]);
+      bool hit;
+      if (d2 < __dmul_rn(t_lo, bb)) {
+        hit = true;
+      } else if (d2 > __dmul_rn(t_hi, bb)) {
+        hit = false;
+      } else {  // hrgen's sequence (generator.py:266)
+        const double dist = __dmul_rn(2.0, asinh(__dsqrt_rn(__ddiv_rn(d2, bb))));
+        hit = dist < R;
+        if (j != i && fabs(dist - R) <= tie) ++nt;
+      }
+      if (hit && j != i) {
+        if (kWrite) idx[at++] = (int32_t)j;
+        else ++cnt;
+      }
+    }
+  }
+  if (ok && !kWrite) deg[i] = cnt;
+  if (kWrite && nt) atomicAdd(ties, nt);
+}
+
 // Compact rows -> the n-row CSR of the API (on request): degrees by vertex
 // id, then every row copied to its place, a warp per row.
 __global__ void __launch_bounds__(256) k_expand_deg(int64_t nq, const int64_t* __restrict__ rp_c,

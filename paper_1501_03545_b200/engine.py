@@ -102,6 +102,16 @@ class Engine:
         self.last_stats = st
         return st
 
+    def edges_brute_force(self, phi, r_poincare, radius: float) -> int:
+        """hrgen generate_brute_force on the device; returns the near-tie count."""
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        r_poincare = np.ascontiguousarray(r_poincare, dtype=np.float64)
+        ties = ctypes.c_int64()
+        _lib.check(self._L.hrg_edges_brute_force(self._ctx, phi.size, phi.ctypes.data,
+                                                 r_poincare.ctypes.data, _lib.MEM_HOST,
+                                                 float(radius), ctypes.byref(ties)))
+        return ties.value
+
     def sample_points(self, model: ModelParams, seed: int, order: int = _lib.ORDER_SAMPLE):
         n = int(model.n)
         phi, rn, rp = (np.empty(n, np.float64) for _ in range(3))

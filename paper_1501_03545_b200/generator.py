@@ -219,11 +219,24 @@ def edges_from_coordinates(coords, radius, *, alpha=1.0, device=None, shard=None
 
 
 def generate_brute_force(coords, radius, *, device=None) -> Graph:
-    """hrgen generator.py:249-274 signature.  hrgen's all-pairs reference and
-    its quadtree generator produce the same edge set (its acceptance
-    criterion 01); here both names evaluate the quadtree edge predicate on the
-    GPU over every candidate pair the band index cannot exclude."""
-    return edges_from_coordinates(coords, radius, device=device)
+    """hrgen generator.py:249-274: all-pairs edges, {i, j} iff
+    2 asinh(sqrt(d2 / (b_i b_j))) < radius, evaluated in hrgen's order on the
+    device (O(n^2); a validation reference, like hrgen's).  Pairs within 4
+    ulps of the radius, where the device's asinh and numpy's may round
+    differently, are counted in `generate_brute_force.last_near_ties`."""
+    if not radius > 0.0:
+        raise ParameterDomainError("radius must be positive")
+    n = len(coords)
+    if n == 0:
+        return Graph.from_edge_arrays(0, [], [])
+    eng = get_engine(device)
+    generate_brute_force.last_near_ties = eng.edges_brute_force(coords.phi, coords.r_poincare,
+                                                                float(radius))
+    indptr, indices = eng.copy_csr(np.int64)
+    return Graph(indptr=indptr, indices=indices)
+
+
+generate_brute_force.last_near_ties = 0
 
 
 def add_long_range_edges(graph: Graph, fraction, seed) -> Graph:

@@ -126,6 +126,31 @@ def test_reference_runs_bit_exact(oracle, run):
     check_csr(g)
 
 
+def _brute_cases():
+    import json
+    import os
+    with open(os.path.join(gd.GOLDEN, "brute.json")) as fh:
+        return json.load(fh)
+
+
+def test_brute_force_equals_reference_brute_force(oracle):
+    """GPU all-pairs path == hrgen.generate_brute_force (fixtures made by
+    running it, tests/golden/make_brute_golden.py) on 146 golden runs."""
+    cases = _brute_cases()
+    assert len(cases) >= 140
+    runs = gd.runs()
+    ties = 0
+    for case in cases:
+        run = runs[case["run"]]
+        coords = VertexCoordinates(phi=run.phi, r_native=None, r_poincare=run.r_poincare)
+        g = P.generate_brute_force(coords, run.R)
+        ties += P.generate_brute_force.last_near_ties
+        assert g.m == case["m"], case
+        assert edge_set_hash(oracle, g) == case["edge_sha256"], case
+        check_csr(g)
+    print(f"[brute] {len(cases)} runs, near ties {ties}")
+
+
 def test_config0_edges_exact():
     run = gd.runs(["config0"])[0]
     coords = VertexCoordinates(phi=run.phi, r_native=None, r_poincare=run.r_poincare)
