@@ -395,7 +395,19 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   // round trip (buffers sized by upper bounds, counts read on the device);
   // one synchronisation at the end checks for a staging overflow, in which
   // case the pass is re-run with the capacity the bump allocator reached.
-  if (c->stage_cap == 0) c->stage_cap = std::max<int64_t>(64 * np, 1 << 20);
+  if (c->stage_cap == 0) {
+    // first call on this context: the model's expected degree (hrgen
+    // geometry.py:170-190, power-law regime) with 30% headroom, so dense
+    // graphs do not void their first pass
+    int64_t cap = std::max<int64_t>(64 * np, 1 << 20);
+    if (M->alpha > 0.5) {
+      double kexp = 0.0;
+      if (hrg_expected_avg_degree(M->n, M->alpha, M->R, &kexp) == HRG_OK && std::isfinite(kexp) &&
+          kexp > 0.0)
+        cap = std::max<int64_t>(cap, (int64_t)(1.3 * kexp * (double)np) + (1 << 20));
+    }
+    c->stage_cap = cap;
+  }
   unsigned long long ctr[16];
   int64_t nnz = 0, total_chunks = 0;
   for (int attempt = 0; attempt < 3; ++attempt) {
