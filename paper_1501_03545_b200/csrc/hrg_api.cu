@@ -349,6 +349,12 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   }
 
   if (c->grid_light == 0) {
+#ifdef HRG_LIGHT_CARVEOUT
+    for (auto kern : {k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>,
+                      k_light<false, kSegCap, HRG_LIGHT_MINBLOCKS>})
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    HRG_LIGHT_CARVEOUT));
+#endif
     c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, kWideMinBlocks>, kLightThreads);
     c->grid_light_shard =
