@@ -361,6 +361,11 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
         occupancy_grid(c, k_light<true, kSegCapShard, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact_heavy = occupancy_grid(c, k_compact_heavy);
+#ifdef HRG_COMPACT_CARVEOUT
+    for (auto kern : {k_compact_light<true>, k_compact_light<false>})
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    HRG_COMPACT_CARVEOUT));
+#endif
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSortWarpSmem));
