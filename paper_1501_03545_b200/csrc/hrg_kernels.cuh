@@ -1187,14 +1187,15 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
   const int wb = tid - lane;  // first thread of this warp
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long cand_local = 0;
   // tiles handed out dynamically (their cost varies by orders of magnitude
   // between inner and outer bands): first one by warp id, then a counter
-  int64_t tk = wid;
+  // every tile from the counter, the first one included: a block that only
+  // becomes resident late (the grid may exceed what fits beside the shared
+  // carve-out) must not hold back a tile from the head of the list
+  int64_t tk = __shfl_sync(FULL, lane == 0 ? (int64_t)atomicAdd(A.tile_next, 1ull) : 0, 0);
   for (; tk < A.ntiles;
-       tk = __shfl_sync(FULL, lane == 0 ? (int64_t)(nw + atomicAdd(A.tile_next, 1ull)) : 0, 0)) {
+       tk = __shfl_sync(FULL, lane == 0 ? (int64_t)atomicAdd(A.tile_next, 1ull) : 0, 0)) {
     const uint64_t tv = __ldg(A.tiles + tk);
     if (tv == ~0ull) break;
     const int32_t v0 = (int32_t)(tv & 0xffffffffu) + lane;
