@@ -1158,7 +1158,10 @@ constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | l
 #endif
 constexpr int kSegCapWide = HRG_WIDE_CAP;   // static shared memory stays under 48 KB
 constexpr int kWideMinBlocks = HRG_WIDE_MINB;
-constexpr int kSegCapShard = 24;  // sharded runs (few tiles per warp)
+#ifndef HRG_SEGCAP_SHARD
+#define HRG_SEGCAP_SHARD 24
+#endif
+constexpr int kSegCapShard = HRG_SEGCAP_SHARD;  // sharded runs (few tiles per warp)
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
 struct LightSmem {
