@@ -1512,10 +1512,13 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t total_chunks = *A.total_chunks;
-  for (int64_t c = warp; c < total_chunks; c += nwarps) {
+  // chunks from a counter (tile_next[2]): a hub's chunks cost far more than
+  // a barely-deferred query's, and a static stride left the pass in its tail
+  auto next_chunk = [&]() {
+    return __shfl_sync(FULL, lane == 0 ? (int64_t)atomicAdd(A.tile_next + 2, 1ull) : 0, 0);
+  };
+  for (int64_t c = next_chunk(); c < total_chunks; c = next_chunk()) {
     const int64_t e = __ldg(A.chunk_entry + c);
     const int32_t v = A.heavy_v[e];
     const int64_t local = c - A.chunk_start[e];
