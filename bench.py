@@ -79,6 +79,10 @@ def parse():
     ap.add_argument("--sweep", action="store_true",
                     help="config 4: one line per (k, gamma) point of the density/exponent "
                          "sweep at n=1e7, seed 4 (evidence runs, not the driver's line)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="print each rank's shard plan without GPU work (launcher test)")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the whole-graph CPU reference run and edge-set comparison")
     ap.add_argument("--shard-sim", type=int, default=0, metavar="N",
                     help="time each of N angular shards in turn on this one GPU and report "
                          "the per-shard times and their max (stand-in for an N-GPU run)")
@@ -174,6 +178,29 @@ def cpu_reference_step(params, model, consts, n_queries, nthreads):
                                t_query_sample_s=tm.t_query_s, queries=nq, m_est=m_est)
 
 
+def cpu_reference_whole(params, model, consts, phi, rp, nthreads, want_pairs):
+    """The reference algorithm on the host for the WHOLE graph, no
+    extrapolation: the oracle's Philox sampler + hrgen's inverse CDF for all
+    n points (timed, as hrgen samples its own points), then the polar
+    quadtree (hrgen quadtree.py build/pack/query_many, libm trig) over the
+    GPU's coordinates -- same point set as the GPU run, so its edge set is
+    the parity reference -- with every vertex queried."""
+    from oracle import oracle as O
+    n = model.n
+    t0 = time.perf_counter()
+    u1, u2 = O.philox_uniforms(n, params["seed"])
+    O.sample_from_uniforms(u1, u2, consts["two_over_alpha"], consts["sinh_half_alpha_r"],
+                           consts["r_cap"], consts["rp_cap"])
+    t_sample = time.perf_counter() - t0
+    del u1, u2
+    pairs, m, tm = O.edges_quadtree(phi, rp, consts["cosh_r_minus_1"], model.alpha,
+                                    consts["max_r"], 512, O.TRIG_LIBM, nthreads,
+                                    want_pairs=want_pairs)
+    t = t_sample + tm.t_build_s + tm.t_query_s
+    return m / t, pairs, dict(t_sample_s=t_sample, t_build_s=tm.t_build_s,
+                              t_query_s=tm.t_query_s, t_total_s=t, m=m)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -259,11 +286,11 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    launches, cand, nnz = 0, 0, 0
+    cand, nnz = 0, 0
     phases = {}
+    l0 = eng.launches()
     for _ in range(args.steps):
         st = eng.generate(model, params["seed"], order, shard)
-        launches += st.kernel_launches
         cand, nnz = st.candidates, st.nnz
         for k in ("t_sample_ms", "t_sort_ms", "t_build_ms", "t_light_ms", "t_heavy_ms",
                   "t_compact_ms", "t_rowsort_ms", "t_edges_ms"):
@@ -271,6 +298,7 @@ def run_ours(args):
         phases.setdefault("heavy_queries", []).append(st.heavy_queries)
     e1.record()
     torch.cuda.synchronize()
+    launches = eng.launches() - l0  # this library's kernels only (CUB sort/scan not counted)
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / max(args.steps, 1)
@@ -394,18 +422,44 @@ def run_ours(args):
                 "fp64": {"pair_tests": cand_all / world, "flop_per_test": 6,
                          "tflops": cand_all / world * 6 / (tq / 1e3) / 1e12}}
 
-    cpu = None
+    cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
         try:
+            from oracle import oracle as O
             consts = P.model_constants(model.R, model.alpha)
             nthreads = os.cpu_count() or 1
-            v, info = cpu_reference_step(params, model, consts, args.cpu_queries, nthreads)
+            # the graph the timed steps generated, read back with its coordinates
+            with eng.lock:
+                eng.generate(model, params["seed"], order, shard)
+                ip, ix = eng.copy_csr(np.int64, pinned=False)
+                phi, _, rp = eng.copy_coords()
+            v, pairs, info = cpu_reference_whole(params, model, consts, phi, rp, nthreads,
+                                                 want_pairs=not args.no_parity)
+            v_est, est = cpu_reference_step(params, model, consts, args.cpu_queries, nthreads)
             cpu = {"value": v, "unit": UNIT, "cores": nthreads, "kind": "port",
-                   "sample": f"oracle polar quadtree (hrgen algorithm): all {model.n} points "
-                             f"sampled + full tree + {info['queries']} vertex queries, "
-                             f"whole-graph time extrapolated", **info}
+                   "sample": f"the whole graph, no extrapolation: oracle/hrg_oracle.c (hrgen's "
+                             f"polar quadtree restated in C, libm trig) samples all {model.n} "
+                             f"points, builds the tree and answers every vertex query on "
+                             f"{nthreads} host threads",
+                   **info,
+                   "sampled_estimate": {"value": v_est, "queries": est["queries"],
+                                        "how": "full tree + a bounded query sample, "
+                                               "extrapolated linearly in queries"}}
+            if pairs is not None:
+                rows = np.repeat(np.arange(model.n, dtype=np.int64), np.diff(ip))
+                keep = ix > rows
+                got = np.column_stack((rows[keep], ix[keep]))
+                del rows, keep, ix
+                d = O.compare_edge_sets(got, pairs, phi, rp, model.R)
+                parity = {"scope": "whole edge set", "ref": "oracle quadtree (hrgen "
+                          "quadtree.py restated), libm trig = hrgen's arithmetic",
+                          "m_gpu": d["m_got"], "m_ref": d["m_want"],
+                          "mismatches": d["only_got"] + d["only_want"],
+                          "max_rel_gap": d["max_gap"], "outside_band": d["outside_band"],
+                          "band": "|cosh d - cosh R| <= 1e-12 cosh R"}
+                del got, pairs
         except Exception as e:  # pragma: no cover
-            cpu = {"error": str(e)}
+            cpu = {"error": repr(e)}
 
     line = {
         "metric": metric_for(params), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -414,7 +468,7 @@ def run_ours(args):
         "config": config_block(params, model, args, world),
         "m": m_total, "candidates": cand_all,
         "phases_ms": med,
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "clocks": clk,
         "gpu_launches": launches,
     }
     print(json.dumps(line))
@@ -483,8 +537,51 @@ def run_sweep(args):
     return rc
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(args):
+    """`--gpus N` (N > 1) without a torchrun environment: re-run this script
+    under torch.distributed.run with N ranks, one per GPU, rendezvous on
+    127.0.0.1; rank 0 prints the line.  Returns the launcher's exit code."""
+    port = os.environ.get("MASTER_PORT") or str(free_port())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """--dry-run: the rank/shard plan each rank would run (no GPU work);
+    exercised under gloo by tests/test_bench_launcher.py."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    plan = {"rank": rank, "world": world, "shard": [rank, world] if world > 1 else None,
+            "config": config_params(args)}
+    if world > 1:
+        plans = [None] * world
+        dist.all_gather_object(plans, plan)
+        dist.destroy_process_group()
+    else:
+        plans = [plan]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": plans}))
+    return 0
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.sweep:
         return run_sweep(args)
     if args.shard_sim:

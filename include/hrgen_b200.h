@@ -46,6 +46,15 @@ enum {
                              without a sort pass.  Same graph up to relabelling. */
 };
 
+/* sin/cos behind the Poincare coordinates p_x = r cos(phi), p_y = r sin(phi)
+ * (quadtree.py:474-475, 516-517). */
+enum {
+  HRG_TRIG_LIBM = 0,  /* default: glibc 2.39's dbl-64 sin/cos bit for bit -- what
+                         numpy evaluates on x86-64 glibc hosts, i.e. hrgen's own
+                         arithmetic; the edge set is then hrgen's exactly */
+  HRG_TRIG_CR = 1     /* correctly rounded sin/cos (libm-independent) */
+};
+
 /* Memory kinds for user buffers. */
 enum { HRG_MEM_HOST = 0, HRG_MEM_DEVICE = 1 };
 
@@ -95,6 +104,11 @@ const char *hrg_last_error(void);
 hrg_status hrg_context_create(int device, void *cuda_stream, hrg_context **out);
 hrg_status hrg_context_destroy(hrg_context *ctx);
 hrg_status hrg_context_set_stream(hrg_context *ctx, void *cuda_stream);
+/* Trig mode (HRG_TRIG_LIBM, the default, or HRG_TRIG_CR) for later calls. */
+hrg_status hrg_context_set_trig(hrg_context *ctx, int mode);
+/* Kernel launches this library has queued on ctx so far (library kernels
+ * such as CUB's sort and scan passes not included). */
+hrg_status hrg_context_launches(hrg_context *ctx, int64_t *out);
 
 /* hrgen geometry.py:170-190 expected_avg_degree / 197-232 target_radius
  * (libm evaluation; the Python layer uses numpy for bit-identical R). */
@@ -152,17 +166,6 @@ hrg_status hrg_result_device_ptrs(hrg_context *ctx, const double **phi, const do
 /* Pinned host memory helpers (for callers without a CUDA runtime binding). */
 hrg_status hrg_host_alloc(size_t bytes, void **out);
 hrg_status hrg_host_free(void *p);
-
-/* Diagnostic: the device's correctly rounded sin/cos (the values behind
- * p_x = r*cos(phi), quadtree.py:474) for n host angles in [0, 2pi). */
-hrg_status hrg_debug_sincos(hrg_context *ctx, int64_t n, const double *x, double *s, double *c);
-
-/* Diagnostic: the sampler-side fast sin/cos (table + short series + rounding
- * test) against the full double-double evaluation on n seeded angles (every
- * 4th within 2^-20 of a multiple of pi/4): values that differ, and values
- * the fast path's rounding test sent to the full evaluation. */
-hrg_status hrg_debug_sincos_compare(hrg_context *ctx, int64_t n, uint64_t seed,
-                                    int64_t *mismatches, int64_t *rejected);
 
 /* Wait for all work queued by ctx. */
 hrg_status hrg_synchronize(hrg_context *ctx);

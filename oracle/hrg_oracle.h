@@ -72,6 +72,11 @@ int64_t orc_rows_brute(int64_t n, const double *phi, const double *rp, double a,
                        int nthreads, int64_t nq, const int64_t *qids, int64_t cap,
                        int64_t *indptr, int64_t *indices);
 
+/* |cosh d - cosh R| / cosh R for pairs (u[k], v[k]), in __float128 (the
+ * north star's exception band for pairs on which two edge sets differ). */
+void orc_cosh_gap(int64_t m, const int64_t *u, const int64_t *v, const double *phi,
+                  const double *rp, double R, double *gap);
+
 /* hrgen graph.py:52-77 Graph.from_edge_arrays for u<v pairs: symmetric CSR,
  * rows sorted.  indptr has n+1 entries, indices 2m. */
 void orc_csr_from_pairs(int64_t n, int64_t m, const int64_t *u, const int64_t *v,

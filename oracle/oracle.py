@@ -62,6 +62,7 @@ def lib():
                                      _i64p]
         L.orc_rows_brute.restype = ctypes.c_int64
         L.orc_csr_from_pairs.argtypes = [ctypes.c_int64, ctypes.c_int64, _i64p, _i64p, _i64p, _i64p]
+        L.orc_cosh_gap.argtypes = [ctypes.c_int64, _i64p, _i64p, _d, _d, ctypes.c_double, _d]
         _lib = L
     return _lib
 
@@ -188,6 +189,48 @@ def csr_from_pairs(n, pairs):
     lib().orc_csr_from_pairs(n, m, _p(u, _i64p), _p(v, _i64p), _p(indptr, _i64p),
                              _p(indices, _i64p))
     return indptr, indices
+
+
+def cosh_gap(pairs, phi, rp, R):
+    """|cosh d - cosh R| / cosh R of each (u, v) pair, in __float128."""
+    pairs = np.ascontiguousarray(pairs, dtype=np.int64).reshape(-1, 2)
+    u = np.ascontiguousarray(pairs[:, 0])
+    v = np.ascontiguousarray(pairs[:, 1])
+    phi, rp = _f64(phi), _f64(rp)
+    gap = np.empty(u.size, np.float64)
+    if u.size:
+        lib().orc_cosh_gap(u.size, _p(u, _i64p), _p(v, _i64p), _p(phi), _p(rp), float(R), _p(gap))
+    return gap
+
+
+def compare_edge_sets(got, want, phi, rp, R, band=1e-12):
+    """Exact comparison of two lexicographically sorted (m, 2) u<v edge
+    arrays.  Returns a dict: m of each, the pairs only in one of them, and
+    their largest cosh-distance gap (the north star allows differences only
+    where |cosh d - cosh R| <= band * cosh R)."""
+    got = np.ascontiguousarray(got, dtype=np.int64).reshape(-1, 2)
+    want = np.ascontiguousarray(want, dtype=np.int64).reshape(-1, 2)
+    n = int(max(got.max(initial=-1), want.max(initial=-1))) + 1
+    if got.shape == want.shape and np.array_equal(got, want):
+        return dict(m_got=len(got), m_want=len(want), only_got=0, only_want=0, max_gap=0.0,
+                    outside_band=0, pairs=np.empty((0, 2), np.int64))
+    kg = got[:, 0] * n + got[:, 1]   # both ascending (lexicographic order)
+    kw = want[:, 0] * n + want[:, 1]
+
+    def missing(a, b):  # elements of sorted a absent from sorted b
+        if b.size == 0:
+            return a
+        i = np.minimum(np.searchsorted(b, a), b.size - 1)
+        return a[b[i] != a]
+
+    only_g = missing(kg, kw)
+    only_w = missing(kw, kg)
+    diff = np.concatenate([only_g, only_w])
+    pairs = np.column_stack((diff // n, diff % n))
+    gap = cosh_gap(pairs, phi, rp, R)
+    return dict(m_got=len(got), m_want=len(want), only_got=int(only_g.size),
+                only_want=int(only_w.size), max_gap=float(gap.max(initial=0.0)),
+                outside_band=int(np.count_nonzero(gap > band)), pairs=pairs)
 
 
 def edge_hash(pairs):

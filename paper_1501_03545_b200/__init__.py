@@ -8,6 +8,7 @@ no CPU fallback: without libhrgen_b200.so or a CUDA device every generating
 call raises NativeLibraryError.
 """
 
+from ._lib import TRIG_CR, TRIG_LIBM
 from .engine import Engine, Shard, get_engine
 from .errors import (
     InfeasibleParametersError,
@@ -46,7 +47,8 @@ __version__ = "0.1.0"
 __all__ = [
     "DEFAULT_GENERATOR_CAPACITY", "Engine", "GenerationStats", "GeneratorParams", "Graph",
     "InfeasibleParametersError", "InsufficientDataError", "ModelParams", "NativeLibraryError",
-    "OutOfBoundsError", "ParameterDomainError", "Shard", "TWO_PI", "VertexCoordinates",
+    "OutOfBoundsError", "ParameterDomainError", "Shard", "TRIG_CR", "TRIG_LIBM", "TWO_PI",
+    "VertexCoordinates",
     "add_long_range_edges", "alpha_from_gamma", "edges_from_coordinates", "expected_avg_degree",
     "generate", "generate_brute_force", "generate_with_stats", "get_engine", "model_constants",
     "radial_inverse_cdf", "sample_points", "target_radius", "to_native_radius",

@@ -30,15 +30,20 @@ ORDER_SAMPLE = 0
 ORDER_ANGULAR = 1
 MEM_HOST = 0
 MEM_DEVICE = 1
+TRIG_LIBM = 0   # glibc's sin/cos bit for bit (hrgen's arithmetic; the default)
+TRIG_CR = 1     # correctly rounded sin/cos
 
-# every symbol the header declares (checked by tests/test_abi.py)
+# every symbol include/hrgen_b200.h declares, then include/hrgen_b200_debug.h's
+# (checked against the headers by tests/test_abi.py)
 EXPORTED = (
     "hrg_version", "hrg_last_error", "hrg_context_create", "hrg_context_destroy",
-    "hrg_context_set_stream", "hrg_expected_avg_degree", "hrg_target_radius", "hrg_model_init",
-    "hrg_generate", "hrg_sample_points", "hrg_edges_from_coords", "hrg_result_sizes",
-    "hrg_copy_result", "hrg_result_device_ptrs", "hrg_host_alloc", "hrg_host_free",
-    "hrg_synchronize", "hrg_debug_sincos", "hrg_debug_sincos_compare", "hrg_edges_brute_force",
+    "hrg_context_set_stream", "hrg_context_set_trig", "hrg_context_launches",
+    "hrg_expected_avg_degree",
+    "hrg_target_radius", "hrg_model_init", "hrg_generate", "hrg_sample_points",
+    "hrg_edges_from_coords", "hrg_edges_brute_force", "hrg_result_sizes", "hrg_copy_result",
+    "hrg_result_device_ptrs", "hrg_host_alloc", "hrg_host_free", "hrg_synchronize",
 )
+EXPORTED_DEBUG = ("hrg_debug_sincos", "hrg_debug_sincos_compare")
 
 
 class Model(ctypes.Structure):
@@ -83,6 +88,8 @@ def _declare(L):
         "hrg_context_create": (S, [ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
         "hrg_context_destroy": (S, [_vp]),
         "hrg_context_set_stream": (S, [_vp, _vp]),
+        "hrg_context_set_trig": (S, [_vp, ctypes.c_int]),
+        "hrg_context_launches": (S, [_vp, _i64p]),
         "hrg_expected_avg_degree": (S, [ctypes.c_int64, ctypes.c_double, ctypes.c_double, _dp]),
         "hrg_target_radius": (S, [ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_double, _dp]),
@@ -102,7 +109,7 @@ def _declare(L):
         "hrg_host_alloc": (S, [ctypes.c_size_t, ctypes.POINTER(_vp)]),
         "hrg_host_free": (S, [_vp]),
         "hrg_synchronize": (S, [_vp]),
-        "hrg_debug_sincos": (S, [_vp, ctypes.c_int64, _vp, _vp, _vp]),
+        "hrg_debug_sincos": (S, [_vp, ctypes.c_int64, _vp, ctypes.c_int, _vp, _vp]),
         "hrg_debug_sincos_compare": (S, [_vp, ctypes.c_int64, ctypes.c_uint64, _vp, _vp]),
         "hrg_edges_brute_force": (S, [_vp, ctypes.c_int64, _vp, _vp, ctypes.c_int, ctypes.c_double,
                                       _vp]),

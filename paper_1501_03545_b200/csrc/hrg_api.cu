@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/hrgen_b200.h"
+#include "../../include/hrgen_b200_debug.h"
 #include "hrg_kernels.cuh"
 
 using namespace hrg;
@@ -106,6 +107,9 @@ struct hrg_context {
   cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
   unsigned char* h_rb = nullptr;  // mapped pinned readback area (kReadback bytes)
   unsigned char* d_rb = nullptr;  // its device alias
+  int64_t launches = 0;  // this library's kernel launches (CUB's not included)
+  int trig = kTrigLibm;  // sin/cos of the Poincare coordinates (hrg_context_set_trig)
+  int grid_block_count = 0, grid_block_write = 0;
   int grid_light = 0, grid_light_wide = 0, grid_light_shard = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
@@ -178,7 +182,7 @@ __global__ void k_readback(RbItem a, RbItem b, RbItem e, unsigned char* dst) {
 hrg_status readback(hrg_context* c, const void* src_a, size_t na, void* dst_a,
                     const void* src_b = nullptr, size_t nb = 0, void* dst_b = nullptr,
                     const void* src_e = nullptr, size_t ne = 0, void* dst_e = nullptr) {
-  k_readback<<<1, 128, 0, c->stream>>>(RbItem{src_a, na}, RbItem{src_b, nb}, RbItem{src_e, ne},
+  ++c->launches, k_readback<<<1, 128, 0, c->stream>>>(RbItem{src_a, na}, RbItem{src_b, nb}, RbItem{src_e, ne},
                                        c->d_rb);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -216,16 +220,16 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
   unsigned long long* band_pmin = c->band_pmin.as<unsigned long long>();
   CUDA_TRY(cudaMemsetAsync(band_pmin, 0xff, 8 * kMaxBands, st));
   if (sample_ids)
-    k_gather<true><<<blocks_for(n), 256, 0, st>>>(
+    ++c->launches, k_gather<true><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
         c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, nullptr,
         nullptr, c->sh_sampled ? c->sh_gid.as<int32_t>() : nullptr, c->vals_out.as<int32_t>(),
-        band_pmin);
+        band_pmin, c->trig);
   else
-    k_gather<false><<<blocks_for(n), 256, 0, st>>>(
+    ++c->launches, k_gather<false><<<blocks_for(n), 256, 0, st>>>(
         n, c->vals_out.as<int32_t>(), c->k32_out.as<uint32_t>(), c->keys_out.as<uint64_t>(), C,
         c->pr.as<double2>(), c->rn.as<double>(), M->cosh_r_minus_1, recs, q, c->s_rp.as<double>(),
-        c->s_rn.as<double>(), nullptr, nullptr, band_pmin);
+        c->s_rn.as<double>(), nullptr, nullptr, band_pmin, c->trig);
   uint64_t qlo = 0, qhi = (uint64_t)1 << kQBits;
   if (shard && shard->count > 1) {
     // sector bounds on the sort granularity (multiples of 2^kSortShift)
@@ -237,20 +241,20 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
     qlo <<= kSortShift;
     qhi <<= kSortShift;
   }
-  k_band_setup<<<1, 1024, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
+  ++c->launches, k_band_setup<<<1, 1024, 0, st>>>(c->keys_out.as<uint64_t>(), n, L, qlo, qhi, c->bands.as<Band>(),
                                  c->dir_total.as<int64_t>(), c->np < M->n ? c->sh_cover : nullptr,
                                  band_pmin);
   CUDA_TRY(c->dir_gaps.ensure(sizeof(DirGap) * (size_t)(n / 16 + 2 * kMaxBands + 8)));
   unsigned* ngaps = reinterpret_cast<unsigned*>(c->dir_total.as<char>() + 8);
   CUDA_TRY(cudaMemsetAsync(ngaps, 0, 4, st));
-  k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
+  ++c->launches, k_dir_fill<<<blocks_for(n), 256, 0, st>>>(n, c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
                                             c->dir.as<int32_t>(), c->dir_gaps.as<DirGap>(), ngaps);
   const bool sharded = c->np < M->n;
   const ShardRanges R{c->sh_lo, c->sh_hi, c->sh_mode};
-  k_dir_gaps<<<4 * c->sm_count, 256, 0, st>>>(c->dir_gaps.as<DirGap>(), ngaps,
+  ++c->launches, k_dir_gaps<<<4 * c->sm_count, 256, 0, st>>>(c->dir_gaps.as<DirGap>(), ngaps,
                                               c->bands.as<Band>(), c->dir.as<int32_t>(), R,
                                               sharded);
-  k_dir_tail<<<L, 256, 0, st>>>(c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
+  ++c->launches, k_dir_tail<<<L, 256, 0, st>>>(c->keys_out.as<uint64_t>(), c->bands.as<Band>(),
                                 c->dir.as<int32_t>(), R, sharded);
   CUDA_TRY(cudaGetLastError());
   return HRG_OK;
@@ -316,7 +320,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(c->row_ids.ensure(4 * (size_t)np));
     CUDA_TRY(c->rowptr_c.ensure(8 * (size_t)(np + 1)));
     CUDA_TRY(c->nq_buf.ensure(8));
-    k_rowidx<<<4 * c->sm_count, 256, 0, st>>>(A.bands, L, c->vals_out.as<int32_t>(),
+    ++c->launches, k_rowidx<<<4 * c->sm_count, 256, 0, st>>>(A.bands, L, c->vals_out.as<int32_t>(),
                                               c->rowidx.as<int32_t>(), c->row_ids.as<int32_t>(),
                                               c->nq_buf.as<int64_t>());
     A.rowidx = c->rowidx.as<int32_t>();
@@ -330,9 +334,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   CUDA_TRY(c->wtab.ensure(sizeof(float) * (size_t)rows * L));
   A.wtab = c->wtab.as<float>();
   A.wrows = rows;
-  k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->cosh_r_minus_1,
+  ++c->launches, k_window_table<<<rows, 32, 0, st>>>(A.bands, L, rows, M->cosh_r_minus_1,
                                       std::ldexp(1.0, -45), c->wtab.as<float>());
-  int launches = 1;
 
   // query tiles: 32 consecutive positions of one band, band after band
   // (interleaving the bands' tiles by angle cuts DRAM reads by 40% but
@@ -341,11 +344,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     const int64_t ntmax = np / 32 + L + 1;
     CUDA_TRY(c->tk0.ensure(8 * (size_t)ntmax));
     CUDA_TRY(c->tv0.ensure(8 * (size_t)ntmax));
-    k_tile_keys<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
+    ++c->launches, k_tile_keys<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
         A.bands, L, A.keys, ntmax, c->tk0.as<uint64_t>(), c->tv0.as<uint64_t>());
     A.tiles = c->tv0.as<uint64_t>();
     A.ntiles = ntmax;
-    launches += 1;
   }
 
   if (c->grid_light == 0) {
@@ -367,6 +369,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                     HRG_COMPACT_CARVEOUT));
 #endif
     c->grid_compact = occupancy_grid(c, k_compact_light<true>, kCompactThreads);
+    c->grid_block_count = occupancy_grid(c, k_block<true, false>, kBlockThreads);
+    c->grid_block_write = occupancy_grid(c, k_block<true, true>, kBlockThreads);
     CUDA_TRY(cudaFuncSetAttribute(k_sort_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kSortWarpSmem));
     CUDA_TRY(cudaFuncSetAttribute(k_sort_rows<256, kBucketMax, kMidShift>,
@@ -376,6 +380,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sort_rows_smem<kLargeMax, 2>()));
   }
+  // range query: dense blocks (count pass + write pass, hrg_block.cuh; the
+  // default) or the per-query window walk (k_light + staging + compaction)
+  bool block = true;
+  if (const char* e = getenv("HRG_QUERY")) block = strcmp(e, "walk") != 0;
   // segment slots per light query: the wide variant when most of the 32
   // bands hold points (expected >= 1 point per band, from the radial CDF
   // (cosh(alpha r) - 1) / (cosh(alpha R) - 1)), so light queries reach them all
@@ -444,22 +452,30 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * nrows, st));
     CUDA_TRY(cudaMemsetAsync(c->counters.p, 0, 128, st));
     CUDA_TRY(cudaEventRecord(c->ev[E_INDEXED], st));
-    {
+    if (block) {
+      // count pass of the block range query (hrg_block.cuh)
+      const unsigned gbc = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>(blocks_for(np, kBlockThreads), c->grid_block_count));
+      if (sample_ids)
+        ++c->launches, k_block<true, false><<<gbc, kBlockThreads, 0, st>>>(A, rowbuf, nrows, nullptr, 0, SortJobs{});
+      else
+        ++c->launches, k_block<false, false><<<gbc, kBlockThreads, 0, st>>>(A, rowbuf, nrows, nullptr, 0, SortJobs{});
+    } else {
       constexpr int MB = HRG_LIGHT_MINBLOCKS;
       if (sample_ids && shard_slots)
-        k_light<true, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (shard_slots) k_light<false, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (sample_ids && !wide) k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (!wide) k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (sample_ids) k_light<true, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
-      else k_light<false, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
+        ++c->launches, k_light<true, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (shard_slots) ++c->launches, k_light<false, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (sample_ids && !wide) ++c->launches, k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (!wide) ++c->launches, k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      else if (sample_ids) ++c->launches, k_light<true, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
+      else ++c->launches, k_light<false, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
     }
     CUDA_TRY(cudaEventRecord(c->ev[E_PLANNED], st));
-    k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),
+    ++c->launches, k_heavy_prep<<<1, 1024, 0, st>>>(A.heavy_c, A.heavy_n, c->nchunks.as<int32_t>(),
                                      c->chunk_start.as<int64_t>(), c->chunk_entry.as<int32_t>(),
                                      d_chunks, A.overflow);
-    if (sample_ids) k_heavy<true><<<c->grid_heavy, 256, 0, st>>>(A, 0);
-    else k_heavy<false><<<c->grid_heavy, 256, 0, st>>>(A, 0);
+    if (sample_ids) ++c->launches, k_heavy<true><<<c->grid_heavy, 256, 0, st>>>(A, 0);
+    else ++c->launches, k_heavy<false><<<c->grid_heavy, 256, 0, st>>>(A, 0);
     CUDA_TRY(cudaEventRecord(c->ev[E_COUNTED], st));
     CUDA_TRY(cudaGetLastError());
     hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), rowbuf, nrows);
@@ -504,13 +520,24 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     G.cur = c->sub_cur.as<unsigned long long>();
     J.giant = G.rows;
     CUDA_TRY(cudaEventRecord(c->ev[E_WRITE0], st));
-    if (sample_ids) k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
-    else k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
-    k_scan_chunks<<<1, 1024, 0, st>>>(c->chunk_hits.as<int32_t>(), d_chunks,
+    if (block) {
+      // write pass: rows straight into the CSR (light rows sorted on the way)
+      const unsigned gbw = (unsigned)std::max<int64_t>(
+          1, std::min<int64_t>(blocks_for(np, kBlockThreads), c->grid_block_write));
+      if (sample_ids)
+        ++c->launches, k_block<true, true><<<gbw, kBlockThreads, 0, st>>>(A, rp, nrows, idx, cap, J);
+      else
+        ++c->launches, k_block<false, true><<<gbw, kBlockThreads, 0, st>>>(A, rp, nrows, idx, cap, J);
+    } else if (sample_ids) {
+      ++c->launches, k_compact_light<true><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
+    } else {
+      ++c->launches, k_compact_light<false><<<gc, kCompactThreads, 0, st>>>(A, rp, idx, J);
+    }
+    ++c->launches, k_scan_chunks<<<1, 1024, 0, st>>>(c->chunk_hits.as<int32_t>(), d_chunks,
                                       c->chunk_off.as<int64_t>(), A.overflow);
-    k_compact_heavy<<<c->grid_compact_heavy, 256, 0, st>>>(A, 0, c->chunk_off.as<int64_t>(), rp, idx,
+    ++c->launches, k_compact_heavy<<<c->grid_compact_heavy, 256, 0, st>>>(A, 0, c->chunk_off.as<int64_t>(), rp, idx,
                                                    sample_ids);
-    if (sample_ids) k_queue_heavy_rows<<<2 * c->sm_count, 256, 0, st>>>(A, rp, J);
+    if (sample_ids) ++c->launches, k_queue_heavy_rows<<<2 * c->sm_count, 256, 0, st>>>(A, rp, J);
     CUDA_TRY(cudaEventRecord(c->ev[E_WRITTEN], st));
     c->idx_final = idx;
     if (sample_ids) {
@@ -527,17 +554,17 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       CUDA_TRY(cudaEventRecord(c->fork, st));
       CUDA_TRY(cudaStreamWaitEvent(s1, c->fork, 0));
       CUDA_TRY(cudaStreamWaitEvent(s2, c->fork, 0));
-      k_sort_warp<<<HRG_SORT_GRID * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
-      k_sort_rows<256, kBucketMax, kMidShift>
+      ++c->launches, k_sort_warp<<<HRG_SORT_GRID * sm, kSortWarpThreads, kSortWarpSmem, st>>>(idx, J);
+      ++c->launches, k_sort_rows<256, kBucketMax, kMidShift>
           <<<HRG_SORT_GRID * sm, 256, sort_rows_smem<kBucketMax, kMidShift>(), s1>>>(idx, idx, J.mid,
                                                                                 J.large);
-      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
+      ++c->launches, k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
           idx, idx, J.large, G.rows);
-      k_giant_plan<<<1, 1024, 0, s2>>>(G);
-      k_giant_hist<<<2 * sm, 1024, 0, s2>>>(idx, G, n);
-      k_giant_scan<<<sm, 1024, 0, s2>>>(G);
-      k_giant_scatter<<<2 * sm, 1024, 0, s2>>>(idx, c->idx2.as<int32_t>(), G, n);
-      k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
+      ++c->launches, k_giant_plan<<<1, 1024, 0, s2>>>(G);
+      ++c->launches, k_giant_hist<<<2 * sm, 1024, 0, s2>>>(idx, G, n);
+      ++c->launches, k_giant_scan<<<sm, 1024, 0, s2>>>(G);
+      ++c->launches, k_giant_scatter<<<2 * sm, 1024, 0, s2>>>(idx, c->idx2.as<int32_t>(), G, n);
+      ++c->launches, k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
           c->idx2.as<int32_t>(), idx, G.sub, none);
       CUDA_TRY(cudaEventRecord(c->join[0], s1));
       CUDA_TRY(cudaEventRecord(c->join[1], s2));
@@ -554,13 +581,20 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     }
     total_chunks = (int64_t)ctr[14];
     if ((ctr[3] & 0xffffffffull) == 0) break;
-    // staging overflowed: size it from the bump allocator's final value
-    c->stage_cap = (int64_t)(ctr[0] + ctr[0] / 8 + 4096);
+    if (ctr[3] & 4) return fail(HRG_ERR_INTERNAL, "block query: write pass disagrees with count pass");
+    // staging (or, block query, the CSR) overflowed: size it from the bump
+    // allocator's final value / the CSR size
+    {
+      const int64_t need = std::max<int64_t>((int64_t)ctr[0], nnz);
+      c->stage_cap = need + need / 8 + 4096;
+    }
     if (attempt == 2) return fail(HRG_ERR_INTERNAL, "staging buffer overflow");
   }
   // next call: keep ~10% headroom over this call's staging use
-  c->stage_cap = std::max<int64_t>(c->stage_cap, (int64_t)(ctr[0] + ctr[0] / 10 + 4096));
-  launches += 9 + (sample_ids ? 9 : 0);  // light, heavy prep+pass, 3 scans, compaction(s), sorts
+  {
+    const int64_t used = std::max<int64_t>((int64_t)ctr[0], nnz);
+    c->stage_cap = std::max<int64_t>(c->stage_cap, used + used / 10 + 4096);
+  }
   c->nnz = nnz;
   c->compact_result = compact;
   if (stats) {
@@ -569,7 +603,6 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     stats->candidates = (int64_t)ctr[1];
     stats->heavy_queries = (int64_t)(ctr[2] & 0xffffffffull);
     stats->heavy_chunks = total_chunks;
-    stats->kernel_launches += launches;
   }
   return HRG_OK;
 }
@@ -587,7 +620,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   CUDA_TRY(c->sh_buf.ensure(1024));
   unsigned long long* d_min = reinterpret_cast<unsigned long long*>(c->sh_buf.p);
   CUDA_TRY(cudaMemsetAsync(d_min, 0xff, 8, st));
-  k_min_rp<<<4 * c->sm_count, 256, 0, st>>>(n, c->pr.as<double2>(), d_min);
+  ++c->launches, k_min_rp<<<4 * c->sm_count, 256, 0, st>>>(n, c->pr.as<double2>(), d_min);
   size_t tb = 0;
   // window table on bands whose innermost radius is their threshold
   std::vector<Band> tbands(L);
@@ -602,7 +635,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   CUDA_TRY(c->sh_wtab.ensure(sizeof(float) * (size_t)rows * L));
   CUDA_TRY(cudaMemcpyAsync(c->sh_bands.p, tbands.data(), sizeof(Band) * L,
                            cudaMemcpyHostToDevice, st));
-  k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
+  ++c->launches, k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
                                       std::ldexp(1.0, -45), c->sh_wtab.as<float>());
   const int64_t span = (int64_t)1 << 27;
   const int64_t sec_lo = ((int64_t)shard->index * span + shard->count - 1) / shard->count;
@@ -614,7 +647,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   int64_t* hi = lo + kMaxBands;
   int* mode = reinterpret_cast<int*>(hi + kMaxBands);
   float* cover = reinterpret_cast<float*>(mode + kMaxBands);
-  k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_min, sec_lo, sec_hi, lo,
+  ++c->launches, k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_min, sec_lo, sec_hi, lo,
                                    hi, mode, cover);
   c->sh_cover = cover;
   c->sh_lo = lo;
@@ -623,7 +656,7 @@ hrg_status shard_subset(hrg_context* c, const hrg_model* M, const BandSpec& S, i
   // directories sized for density (k_band_setup): up to ~4x the global count
   CUDA_TRY(c->dir.ensure(4 * (size_t)((4 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->sh_keep.ensure((size_t)n));
-  k_shard_flags<<<blocks_for(n), 256, 0, st>>>(n, c->k32_in.as<uint32_t>(), lo, hi, mode,
+  ++c->launches, k_shard_flags<<<blocks_for(n), 256, 0, st>>>(n, c->k32_in.as<uint32_t>(), lo, hi, mode,
                                                c->sh_keep.as<uint8_t>());
   // order-preserving compaction of (key, id) into the sort's output buffers,
   // then back
@@ -686,18 +719,18 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
   unsigned* d_cnt = reinterpret_cast<unsigned*>(c->sh_buf.as<char>() + 960);
   CUDA_TRY(cudaMemsetAsync(d_umin, 0xff, 8, st));
   CUDA_TRY(cudaMemsetAsync(d_cnt, 0, 4, st));
-  k_shard_keys<<<8 * c->sm_count, 256, 0, st>>>(n, P, S, c->k32_out.as<uint32_t>(), d_umin);
+  ++c->launches, k_shard_keys<<<8 * c->sm_count, 256, 0, st>>>(n, P, S, c->k32_out.as<uint32_t>(), d_umin);
   const int rows = (int)std::ceil(M->R / (double)kRowStep) + 2;
   CUDA_TRY(c->sh_bands.ensure(sizeof(Band) * L));
   CUDA_TRY(c->sh_wtab.ensure(sizeof(float) * (size_t)rows * L));
-  k_shard_prep<<<1, 32, 0, st>>>(P, S, d_umin, c->sh_bands.as<Band>(), d_pmin);
-  k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
+  ++c->launches, k_shard_prep<<<1, 32, 0, st>>>(P, S, d_umin, c->sh_bands.as<Band>(), d_pmin);
+  ++c->launches, k_window_table<<<rows, 32, 0, st>>>(c->sh_bands.as<Band>(), L, rows, M->cosh_r_minus_1,
                                       std::ldexp(1.0, -45), c->sh_wtab.as<float>());
   int64_t* lo = reinterpret_cast<int64_t*>(c->sh_buf.as<char>() + 64);
   int64_t* hi = lo + kMaxBands;
   int* mode = reinterpret_cast<int*>(hi + kMaxBands);
   float* cover = reinterpret_cast<float*>(mode + kMaxBands);
-  k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_pmin, S.sec_lo, S.sec_hi,
+  ++c->launches, k_shard_ranges<<<1, 1024, 0, st>>>(c->sh_wtab.as<float>(), L, rows, d_pmin, S.sec_lo, S.sec_hi,
                                    lo, hi, mode, cover);
   c->sh_cover = cover;
   c->sh_lo = lo;
@@ -705,10 +738,10 @@ hrg_status shard_sample(hrg_context* c, const hrg_model* M, int L, const hrg_sha
   c->sh_mode = mode;
   CUDA_TRY(c->dir.ensure(4 * (size_t)((4 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->sh_gid.ensure(4 * (size_t)n));
-  k_shard_select<<<blocks_for(n, 256 * kShardPer), 256, 0, st>>>(
+  ++c->launches, k_shard_select<<<blocks_for(n, 256 * kShardPer), 256, 0, st>>>(
       n, L, c->k32_out.as<uint32_t>(), lo, hi, mode, c->k32_in.as<uint32_t>(),
       c->vals_in.as<int32_t>(), c->sh_gid.as<int32_t>(), d_cnt);
-  k_shard_points<<<8 * c->sm_count, 256, 0, st>>>(P, d_cnt, c->sh_gid.as<int32_t>(),
+  ++c->launches, k_shard_points<<<8 * c->sm_count, 256, 0, st>>>(P, d_cnt, c->sh_gid.as<int32_t>(),
                                                   c->pr.as<double2>());
   CUDA_TRY(cudaGetLastError());
   unsigned np = 0;
@@ -735,6 +768,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     stats->alpha = M->alpha;
     stats->n_bands = L;
   }
+  const int64_t launches0 = c->launches;
   CUDA_TRY(cudaEventRecord(c->ev[E_START], st));
   c->sh_sampled = false;
   const bool shard_sampling = !from_coords && shard && shard->count > 1 && sample_ids;
@@ -748,7 +782,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
     // coordinates on request only (hrg_result_device_ptrs); angular order
     // gathers r_native into its sorted copy, so that one is written
-    k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, nullptr,
+    ++c->launches, k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, nullptr,
                                             sample_ids ? nullptr : c->rn.as<double>(), nullptr,
                                             c->k32_in.as<uint32_t>(), c->vals_in.as<int32_t>(),
                                             c->pr.as<double2>());
@@ -757,7 +791,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   } else {
     c->coords_pending = false;
     CUDA_TRY(cudaMemsetAsync(c->bad.p, 0, 4, st));
-    k_keys_from_coords<<<blocks_for(n), 256, 0, st>>>(
+    ++c->launches, k_keys_from_coords<<<blocks_for(n), 256, 0, st>>>(
         n, c->phi.as<double>(), c->rp.as<double>(), M->max_r, C, S, c->rn.as<double>(),
         c->k32_in.as<uint32_t>(), c->vals_in.as<int32_t>(), c->bad.as<int>(),
         c->pr.as<double2>());
@@ -776,7 +810,6 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   }
   s = build_index(c, M, S, L, shard, C, sample_ids);
   if (s != HRG_OK) return s;
-  if (stats) stats->kernel_launches = 7;  // sample/keys, gather, 5 index kernels (+ CUB sort)
   s = emit_edges(c, M, L, C, sample_ids, shard && shard->count > 1 && sample_ids, stats);
   if (s != HRG_OK) return s;
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -792,6 +825,7 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
     stats->t_heavy_ms = ev_ms(c->ev[E_PLANNED], c->ev[E_COUNTED]);
     stats->t_compact_ms = ev_ms(c->ev[E_WRITE0], c->ev[E_WRITTEN]);
     stats->t_rowsort_ms = ev_ms(c->ev[E_WRITTEN], c->ev[E_ROWSORTED]);
+    stats->kernel_launches = (int32_t)(c->launches - launches0);
   }
   return HRG_OK;
 }
@@ -802,7 +836,7 @@ hrg_status expand_rows(hrg_context* c) {
   cudaStream_t st = c->stream;
   const int64_t n = c->n;
   CUDA_TRY(cudaMemsetAsync(c->deg.p, 0, sizeof(int32_t) * n, st));
-  k_expand_deg<<<4 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
+  ++c->launches, k_expand_deg<<<4 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
                                                 c->row_ids.as<int32_t>(), c->deg.as<int32_t>());
   hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
   if (s != HRG_OK) return s;
@@ -810,7 +844,7 @@ hrg_status expand_rows(hrg_context* c) {
   // once the row sorts are done
   CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(c->nnz, 1)));
   int32_t* out = c->idx2.as<int32_t>();
-  k_expand_rows<<<8 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
+  ++c->launches, k_expand_rows<<<8 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
                                                  c->row_ids.as<int32_t>(), c->idx_final,
                                                  c->rowptr.as<int64_t>(), out);
   CUDA_TRY(cudaGetLastError());
@@ -854,7 +888,7 @@ hrg_status hrg_context_create(int device, void* cuda_stream, hrg_context** out) 
     if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
   }
   // the sin/cos table of the fast path (device-global, idempotent)
-  k_sincos_table<<<1, 256, 0, c->stream>>>();
+  ++c->launches, k_sincos_table<<<1, 256, 0, c->stream>>>();
   cudaError_t r = cudaStreamSynchronize(c->stream);
   if (r == cudaSuccess) r = cudaGetLastError();
   if (r != cudaSuccess) { delete c; return fail(HRG_ERR_CUDA, cudaGetErrorString(r)); }
@@ -891,6 +925,20 @@ hrg_status hrg_context_destroy(hrg_context* c) {
 hrg_status hrg_context_set_stream(hrg_context* c, void* s) {
   if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
   c->stream = (cudaStream_t)s;
+  return HRG_OK;
+}
+
+hrg_status hrg_context_launches(hrg_context* c, int64_t* out) {
+  if (!c || !out) return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
+  *out = c->launches;
+  return HRG_OK;
+}
+
+hrg_status hrg_context_set_trig(hrg_context* c, int mode) {
+  if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");
+  if (mode != HRG_TRIG_LIBM && mode != HRG_TRIG_CR)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "trig mode must be HRG_TRIG_LIBM or HRG_TRIG_CR");
+  c->trig = mode;
   return HRG_OK;
 }
 
@@ -983,12 +1031,19 @@ hrg_status hrg_sample_points(hrg_context* c, const hrg_model* M, uint64_t seed, 
   BandSpec S = make_bands(M->R, &L);
   double C = std::ldexp(1.0, kQBits) / kTwoPi;
   SampleParams P{seed, M->two_over_alpha, M->sinh_half_alpha_r, M->r_cap, M->rp_cap, C};
-  k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
+  ++c->launches, k_sample<<<blocks_for(n), 256, 0, st>>>(n, P, S, c->phi.as<double>(), c->rn.as<double>(),
                                           c->rp.as<double>(), c->k32_in.as<uint32_t>(),
                                           c->vals_in.as<int32_t>(), c->pr.as<double2>());
   CUDA_TRY(cudaGetLastError());
   const double *sp = c->phi.as<double>(), *sn = c->rn.as<double>(), *sr = c->rp.as<double>();
   if (order == HRG_ORDER_ANGULAR) {
+    // build_index sizes everything from c->np and reads the shard state of
+    // the previous call: this call indexes all n points, unsharded
+    c->np = n;
+    c->sh_sampled = false;
+    c->sh_cover = nullptr;
+    c->sh_lo = c->sh_hi = nullptr;
+    c->sh_mode = nullptr;
     s = build_index(c, M, S, L, nullptr, C, false);
     if (s != HRG_OK) return s;
     sp = c->s_phi.as<double>(); sn = c->s_rn.as<double>(); sr = c->s_rp.as<double>();
@@ -1040,7 +1095,8 @@ hrg_status hrg_edges_brute_force(hrg_context* c, int64_t n, const double* phi, c
   double* x = c->s_phi.as<double>();
   double* y = c->s_rn.as<double>();
   double* b = c->s_rp.as<double>();
-  k_bf_points<<<blocks_for(n), 256, 0, st>>>(n, c->phi.as<double>(), c->rp.as<double>(), x, y, b);
+  ++c->launches, k_bf_points<<<blocks_for(n), 256, 0, st>>>(n, c->phi.as<double>(), c->rp.as<double>(), x, y, b,
+                                             c->trig);
   const double S = std::sinh(R / 2.0);
   const double t_lo = (S * (1.0 - 1e-9)) * (S * (1.0 - 1e-9));
   const double t_hi = (S * (1.0 + 1e-9)) * (S * (1.0 + 1e-9));
@@ -1048,7 +1104,7 @@ hrg_status hrg_edges_brute_force(hrg_context* c, int64_t n, const double* phi, c
   CUDA_TRY(c->cand.ensure(8));
   unsigned long long* d_ties = c->cand.as<unsigned long long>();
   CUDA_TRY(cudaMemsetAsync(d_ties, 0, 8, st));
-  k_bf_pairs<false><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie,
+  ++c->launches, k_bf_pairs<false><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie,
                                                     c->deg.as<int32_t>(), nullptr, nullptr,
                                                     nullptr);
   s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
@@ -1057,7 +1113,7 @@ hrg_status hrg_edges_brute_force(hrg_context* c, int64_t n, const double* phi, c
   s = readback(c, c->rowptr.as<int64_t>() + n, 8, &nnz);
   if (s != HRG_OK) return s;
   CUDA_TRY(c->idx.ensure(4 * (size_t)std::max<int64_t>(nnz, 1)));
-  k_bf_pairs<true><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie, nullptr,
+  ++c->launches, k_bf_pairs<true><<<blocks_for(n), 256, 0, st>>>(n, x, y, b, t_lo, t_hi, R, tie, nullptr,
                                                    c->rowptr.as<int64_t>(), c->idx.as<int32_t>(),
                                                    d_ties);
   CUDA_TRY(cudaGetLastError());
@@ -1088,7 +1144,7 @@ hrg_status hrg_result_device_ptrs(hrg_context* c, const double** phi, const doub
   if (!c || !c->have_result) return fail(HRG_ERR_NO_RESULT, "no result");
   if ((phi || rn || rp) && c->coords_pending) {
     CUDA_TRY(cudaSetDevice(c->device));
-    k_sample_coords<<<blocks_for(c->n), 256, 0, c->stream>>>(
+    ++c->launches, k_sample_coords<<<blocks_for(c->n), 256, 0, c->stream>>>(
         c->n, c->pending, c->phi.as<double>(), c->rn.as<double>(), c->rp.as<double>());
     CUDA_TRY(cudaGetLastError());
     c->coords_pending = false;
@@ -1134,7 +1190,7 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
       // widen on the device in one pass, then one copy: the copy engine then
       // never waits for SMs (another context's generation may hold them all)
       CUDA_TRY(c->widen.ensure(8 * (size_t)c->nnz));
-      k_widen<<<blocks_for(c->nnz), 256, 0, st>>>(c->nnz, c->idx_final, c->widen.as<int64_t>());
+      ++c->launches, k_widen<<<blocks_for(c->nnz), 256, 0, st>>>(c->nnz, c->idx_final, c->widen.as<int64_t>());
       CUDA_TRY(cudaMemcpyAsync(indices, c->widen.p, 8 * (size_t)c->nnz, k, st));
     }
   }
@@ -1162,7 +1218,7 @@ hrg_status hrg_debug_sincos_compare(hrg_context* c, int64_t n, uint64_t seed,
   CUDA_TRY(b.ensure(16));
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemsetAsync(b.p, 0, 16, st));
-  k_sincos_compare<<<8 * c->sm_count, 256, 0, st>>>(n, seed, b.as<unsigned long long>());
+  ++c->launches, k_sincos_compare<<<8 * c->sm_count, 256, 0, st>>>(n, seed, b.as<unsigned long long>());
   CUDA_TRY(cudaGetLastError());
   unsigned long long h[2];
   CUDA_TRY(cudaMemcpyAsync(h, b.p, 16, cudaMemcpyDeviceToHost, st));
@@ -1172,8 +1228,10 @@ hrg_status hrg_debug_sincos_compare(hrg_context* c, int64_t n, uint64_t seed,
   return HRG_OK;
 }
 
-hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, double* s, double* co) {
-  if (!c || n < 0 || !x || !s || !co) return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
+hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, int mode, double* s,
+                            double* co) {
+  if (!c || n < 0 || !x || !s || !co || mode < 0 || mode > 2)
+    return fail(HRG_ERR_PARAMETER_DOMAIN, "bad arguments");
   if (n == 0) return HRG_OK;
   CUDA_TRY(cudaSetDevice(c->device));
   Buf b;
@@ -1181,7 +1239,7 @@ hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, double* 
   double* d = b.as<double>();
   cudaStream_t st = c->stream;
   CUDA_TRY(cudaMemcpyAsync(d, x, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
-  k_sincos<<<blocks_for(n), 256, 0, st>>>(n, d, d + n, d + 2 * n, false);
+  ++c->launches, k_sincos<<<blocks_for(n), 256, 0, st>>>(n, d, d + n, d + 2 * n, mode);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(s, d + n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(co, d + 2 * n, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));

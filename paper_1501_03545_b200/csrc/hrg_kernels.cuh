@@ -33,6 +33,7 @@
 #include <stdint.h>
 #include <utility>
 #include "hrg_math.cuh"
+#include "hrg_libm_trig.cuh"
 
 namespace hrg {
 
@@ -99,6 +100,18 @@ namespace hrg {
 #endif
 
 constexpr int kMaxBands = 32;     // one warp lane per radial band
+constexpr int kTrigLibm = 0;      // glibc's sin/cos, bit for bit (hrgen's arithmetic; default)
+constexpr int kTrigCR = 1;        // correctly rounded sin/cos
+
+// cos/sin of an angle in [0, 2pi) as the context's trig mode asks
+__device__ __forceinline__ void trig_sincos(int trig, double x, double* sn, double* cs) {
+  if (trig == kTrigLibm) {
+    *sn = libm::sin(x);
+    *cs = libm::cos(x);
+  } else {
+    sincos_crf(x, sn, cs);
+  }
+}
 constexpr int kQBits = 53;
 constexpr uint64_t kQMask = (1ull << kQBits) - 1;
 constexpr double kTwoPi = 6.283185307179586;  // == 2.0 * math.pi (geometry.py:19)
@@ -304,7 +317,8 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
                                                 double* __restrict__ s_rn,
                                                 const int32_t* __restrict__ gid,
                                                 int32_t* ids_out,
-                                                unsigned long long* __restrict__ band_pmin) {
+                                                unsigned long long* __restrict__ band_pmin,
+                                                int trig) {
   // innermost Poincare radius per band (non-negative doubles order like
   // their bits): warp reduction when a warp's points share a band (sorted
   // positions: nearly always), shared memory, one global atomic per band
@@ -340,7 +354,7 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
   const double ph = q2.x, r = q2.y;
   keys_out[p] = ((uint64_t)(k32[p] >> 27) << kQBits) | qkey(ph, C);
   double sn, cs;
-  sincos_crf(ph, &sn, &cs);
+  trig_sincos(trig, ph, &sn, &cs);  // quadtree.py:474-475 / 516-517
   double cr, rad;
   circle_params(r, a, &cr, &rad);
   const double px = __dmul_rn(r, cs), py = __dmul_rn(r, sn);
@@ -1089,6 +1103,27 @@ __device__ __forceinline__ void finish_trim(const uint64_t* keys, RawWin& r, uin
   if (r.sB < r.eB && (kB0 & kQMask) < r.tlB) { ++r.sB; trim_lo(keys, r.sB, r.eB, r.tlB); }
 }
 
+// Band B's part of a union window centred at `mid` with half-width dlt_f
+// (the window table's value, widened by the sub-tile's half span): <= 2
+// sorted-position segments [sA, eA), [sB, eB) with sB >= eA, trimmed to
+// exact angular keys.  Also the heavy pass's per-query window (span 0), so
+// both paths see the same candidates for a deferred query.
+__device__ __forceinline__ void union_window(const QueryArgs& A, const Band& B, double mid,
+                                             float dlt_f, int32_t& sA, int32_t& eA,
+                                             int32_t& sB, int32_t& eB) {
+  RawWin r = raw_window(A, B, mid, dlt_f);
+  const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
+  const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
+  const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
+  finish_trim(A.keys, r, kA0, kA1, kB0);
+  if (r.sB < r.eB && r.sB < r.eA) {  // the window wraps onto itself: whole band
+    r.sA = B.start; r.eA = B.end; r.sB = r.eB = 0;
+  }
+  if (r.eA < r.sA) r.eA = r.sA;
+  if (r.eB < r.sB) r.eB = r.sB;
+  sA = r.sA; eA = r.eA; sB = r.sB; eB = r.eB;
+}
+
 constexpr int kBandGroup = HRG_BAND_GROUP;    // bands resolved together (loads in flight)
 constexpr bool kTrim = HRG_TRIM;              // exact key trim of per-query windows
 constexpr bool kTrimUnion = HRG_TRIM_UNION;   // ... and of the tile's union windows
@@ -1526,7 +1561,7 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
     int32_t sA = 0, eA = 0, sB = 0, eB = 0;
     if (lane < A.L) {
       const float* wrow = wtab_row(A, A.q.rf[v]);
-      band_segments(A, sb[lane], A.q.phi[v], __ldg(wrow + lane), sA, eA, sB, eB);
+      union_window(A, sb[lane], A.q.phi[v], __ldg(wrow + lane), sA, eA, sB, eB);
     }
     const int32_t lenA = eA - sA, cnt = lenA + (eB - sB);
     int32_t incl = cnt;
@@ -2504,11 +2539,13 @@ __global__ void k_queue_heavy_rows(QueryArgs A, const int64_t* __restrict__ rowp
 
 __global__ void __launch_bounds__(256) k_sincos(int64_t n, const double* __restrict__ x,
                                                 double* __restrict__ s, double* __restrict__ c,
-                                                bool slow) {
+                                                int mode) {
+  // mode 0: glibc's sin/cos (the product default), 1: correctly rounded
+  // (fast path + rounding test), 2: correctly rounded, full evaluation
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) {
-    if (slow) sincos_cr(x[i], s + i, c + i);
-    else sincos_crf(x[i], s + i, c + i);
+    if (mode == 2) sincos_cr(x[i], s + i, c + i);
+    else trig_sincos(mode, x[i], s + i, c + i);
   }
 }
 
@@ -2549,11 +2586,11 @@ __global__ void __launch_bounds__(256) k_sincos_compare(int64_t n, uint64_t seed
 __global__ void __launch_bounds__(256) k_bf_points(int64_t n, const double* __restrict__ phi,
                                                    const double* __restrict__ rp,
                                                    double* __restrict__ x, double* __restrict__ y,
-                                                   double* __restrict__ b) {
+                                                   double* __restrict__ b, int trig) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double sn, cs;
-  sincos_crf(phi[i], &sn, &cs);
+  trig_sincos(trig, phi[i], &sn, &cs);
   const double r = rp[i];
   x[i] = __dmul_rn(r, cs);
   y[i] = __dmul_rn(r, sn);
@@ -2641,3 +2678,5 @@ __global__ void __launch_bounds__(256) k_widen(int64_t n, const int32_t* __restr
 }
 
 }  // namespace hrg
+
+#include "hrg_block.cuh"

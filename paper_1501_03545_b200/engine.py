@@ -59,6 +59,11 @@ class Engine:
         self._ctx = ctx
         self._L = L
         self.last_stats: _lib.Stats | None = None
+        # one context = one set of device buffers and one last result: a
+        # generation and the copy of its result must not interleave with
+        # another thread's (hold `lock` across both; the methods take it too)
+        self.lock = threading.RLock()
+        self.trig = _lib.TRIG_LIBM
 
     def __del__(self):
         try:
@@ -69,65 +74,109 @@ class Engine:
             pass
 
     def set_stream(self, stream: int | None):
-        _lib.check(self._L.hrg_context_set_stream(self._ctx, ctypes.c_void_p(stream or 0)))
+        with self.lock:
+            _lib.check(self._L.hrg_context_set_stream(self._ctx, ctypes.c_void_p(stream or 0)))
+
+    def launches(self) -> int:
+        """Kernel launches this engine's context has queued (library kernels
+        such as CUB's not counted)."""
+        out = ctypes.c_int64()
+        _lib.check(self._L.hrg_context_launches(self._ctx, ctypes.byref(out)))
+        return out.value
+
+    def set_trig(self, mode: int):
+        """sin/cos of later calls: _lib.TRIG_LIBM (hrgen's glibc arithmetic,
+        the default) or _lib.TRIG_CR (correctly rounded)."""
+        with self.lock:
+            _lib.check(self._L.hrg_context_set_trig(self._ctx, int(mode)))
+            self.trig = int(mode)
 
     # -- work ---------------------------------------------------------------
     def generate(self, model: ModelParams, seed: int, order: int = _lib.ORDER_SAMPLE,
                  shard: Shard | None = None) -> _lib.Stats:
         st = _lib.Stats()
         sh = _lib.Shard(shard.index, shard.count) if shard else None
-        _lib.check(self._L.hrg_generate(self._ctx, ctypes.byref(make_model(model)),
-                                        ctypes.c_uint64(int(seed)), order,
-                                        ctypes.byref(sh) if sh else None, ctypes.byref(st)))
-        self.last_stats = st
+        with self.lock:
+            _lib.check(self._L.hrg_generate(self._ctx, ctypes.byref(make_model(model)),
+                                            ctypes.c_uint64(int(seed)), order,
+                                            ctypes.byref(sh) if sh else None, ctypes.byref(st)))
+            self.last_stats = st
         return st
 
     def edges_from_coords(self, model: ModelParams, phi, r_poincare,
                           shard: Shard | None = None) -> _lib.Stats:
         st = _lib.Stats()
         sh = _lib.Shard(shard.index, shard.count) if shard else None
-        if hasattr(phi, "data_ptr") and getattr(phi, "is_cuda", False):
-            kind, p_phi, p_rp = _lib.MEM_DEVICE, phi.data_ptr(), r_poincare.data_ptr()
-            keep = None
+        phi, r_poincare, kind = self._coords(phi, r_poincare)
+        if kind == _lib.MEM_DEVICE:
+            p_phi, p_rp = phi.data_ptr(), r_poincare.data_ptr()
+        else:
+            p_phi, p_rp = phi.ctypes.data, r_poincare.ctypes.data
+        with self.lock:
+            _lib.check(self._L.hrg_edges_from_coords(self._ctx, ctypes.byref(make_model(model)),
+                                                     ctypes.c_void_p(p_phi), ctypes.c_void_p(p_rp),
+                                                     kind, ctypes.byref(sh) if sh else None,
+                                                     ctypes.byref(st)))
+            self.last_stats = st
+        return st
+
+    def _coords(self, phi, r_poincare):
+        """Validated coordinate pair: equal length, 1-d, float64, contiguous;
+        CUDA tensors on this engine's device stay on the device (converted
+        there if needed), everything else becomes host numpy arrays."""
+        if getattr(phi, "is_cuda", False) or getattr(r_poincare, "is_cuda", False):
+            import torch
+            dev = torch.device("cuda", self.device)
+            phi = torch.as_tensor(phi, device=dev).to(torch.float64).contiguous()
+            r_poincare = torch.as_tensor(r_poincare, device=dev).to(torch.float64).contiguous()
+            shape_phi, shape_rp = tuple(phi.shape), tuple(r_poincare.shape)
+            kind = _lib.MEM_DEVICE
         else:
             phi = np.ascontiguousarray(phi, dtype=np.float64)
             r_poincare = np.ascontiguousarray(r_poincare, dtype=np.float64)
-            keep = (phi, r_poincare)
-            kind, p_phi, p_rp = _lib.MEM_HOST, phi.ctypes.data, r_poincare.ctypes.data
-        _lib.check(self._L.hrg_edges_from_coords(self._ctx, ctypes.byref(make_model(model)),
-                                                 ctypes.c_void_p(p_phi), ctypes.c_void_p(p_rp),
-                                                 kind, ctypes.byref(sh) if sh else None,
-                                                 ctypes.byref(st)))
-        del keep
-        self.last_stats = st
-        return st
+            shape_phi, shape_rp = phi.shape, r_poincare.shape
+            kind = _lib.MEM_HOST
+        if len(shape_phi) != 1 or shape_phi != shape_rp:
+            from .errors import ParameterDomainError
+            raise ParameterDomainError(
+                f"phi and r_poincare must be 1-d arrays of equal length (got {shape_phi} and "
+                f"{shape_rp})")
+        return phi, r_poincare, kind
 
     def edges_brute_force(self, phi, r_poincare, radius: float) -> int:
         """hrgen generate_brute_force on the device; returns the near-tie count."""
-        phi = np.ascontiguousarray(phi, dtype=np.float64)
-        r_poincare = np.ascontiguousarray(r_poincare, dtype=np.float64)
+        phi, r_poincare, kind = self._coords(phi, r_poincare)
+        if kind == _lib.MEM_DEVICE:
+            phi, r_poincare = phi.cpu().numpy(), r_poincare.cpu().numpy()
         ties = ctypes.c_int64()
-        _lib.check(self._L.hrg_edges_brute_force(self._ctx, phi.size, phi.ctypes.data,
-                                                 r_poincare.ctypes.data, _lib.MEM_HOST,
-                                                 float(radius), ctypes.byref(ties)))
+        with self.lock:
+            _lib.check(self._L.hrg_edges_brute_force(self._ctx, phi.size, phi.ctypes.data,
+                                                     r_poincare.ctypes.data, _lib.MEM_HOST,
+                                                     float(radius), ctypes.byref(ties)))
         return ties.value
 
     def sample_points(self, model: ModelParams, seed: int, order: int = _lib.ORDER_SAMPLE):
         n = int(model.n)
         phi, rn, rp = (np.empty(n, np.float64) for _ in range(3))
-        _lib.check(self._L.hrg_sample_points(self._ctx, ctypes.byref(make_model(model)),
-                                             ctypes.c_uint64(int(seed)), order, _lib.MEM_HOST,
-                                             phi.ctypes.data, rn.ctypes.data, rp.ctypes.data))
+        with self.lock:
+            _lib.check(self._L.hrg_sample_points(self._ctx, ctypes.byref(make_model(model)),
+                                                 ctypes.c_uint64(int(seed)), order, _lib.MEM_HOST,
+                                                 phi.ctypes.data, rn.ctypes.data, rp.ctypes.data))
         return phi, rn, rp
 
     # -- results ------------------------------------------------------------
     def sizes(self):
         n = ctypes.c_int64()
         nnz = ctypes.c_int64()
-        _lib.check(self._L.hrg_result_sizes(self._ctx, ctypes.byref(n), ctypes.byref(nnz)))
+        with self.lock:
+            _lib.check(self._L.hrg_result_sizes(self._ctx, ctypes.byref(n), ctypes.byref(nnz)))
         return n.value, nnz.value
 
     def copy_csr(self, index_dtype=np.int64, pinned=True):
+        with self.lock:
+            return self._copy_csr(index_dtype, pinned)
+
+    def _copy_csr(self, index_dtype, pinned):
         n, nnz = self.sizes()
         alloc = _pinned_empty if pinned else (lambda s, d: np.empty(s, d))
         indptr = alloc(n + 1, np.int64)
@@ -138,6 +187,10 @@ class Engine:
         return indptr, indices
 
     def copy_coords(self, pinned=False):
+        with self.lock:
+            return self._copy_coords(pinned)
+
+    def _copy_coords(self, pinned):
         n, _ = self.sizes()
         alloc = _pinned_empty if pinned else (lambda s, d: np.empty(s, d))
         phi, rn, rp = (alloc(n, np.float64) for _ in range(3))
@@ -151,26 +204,31 @@ class Engine:
         def ptr(a):
             return None if a is None else a.ctypes.data
         ib = indices.dtype.itemsize if indices is not None else 8
-        _lib.check(self._L.hrg_copy_result(self._ctx, _lib.MEM_HOST, ptr(phi), ptr(r_native),
-                                           ptr(r_poincare), ptr(indptr), ptr(indices), ib))
+        with self.lock:
+            _lib.check(self._L.hrg_copy_result(self._ctx, _lib.MEM_HOST, ptr(phi), ptr(r_native),
+                                               ptr(r_poincare), ptr(indptr), ptr(indices), ib))
 
     def device_csr(self):
         """(indptr int64, indices int32) as torch CUDA tensors (device copies)."""
         import torch
-        n, nnz = self.sizes()
-        dev = torch.device("cuda", self.device)
-        indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        indices = torch.empty(max(nnz, 0), dtype=torch.int32, device=dev)
-        _lib.check(self._L.hrg_copy_result(self._ctx, _lib.MEM_DEVICE, None, None, None,
-                                           indptr.data_ptr(), indices.data_ptr(), 4))
+        with self.lock:
+            n, nnz = self.sizes()
+            dev = torch.device("cuda", self.device)
+            indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+            indices = torch.empty(max(nnz, 0), dtype=torch.int32, device=dev)
+            _lib.check(self._L.hrg_copy_result(self._ctx, _lib.MEM_DEVICE, None, None, None,
+                                               indptr.data_ptr(), indices.data_ptr(), 4))
         return indptr, indices
 
-    def debug_sincos(self, x):
+    def debug_sincos(self, x, mode=_lib.TRIG_LIBM):
+        """Device sin/cos of host angles: mode 0 glibc's (the product's
+        default), 1 correctly rounded (fast path), 2 correctly rounded (full)."""
         x = np.ascontiguousarray(x, dtype=np.float64)
         s = np.empty_like(x)
         c = np.empty_like(x)
-        _lib.check(self._L.hrg_debug_sincos(self._ctx, x.size, x.ctypes.data, s.ctypes.data,
-                                            c.ctypes.data))
+        with self.lock:
+            _lib.check(self._L.hrg_debug_sincos(self._ctx, x.size, x.ctypes.data, int(mode),
+                                                s.ctypes.data, c.ctypes.data))
         return s, c
 
     def debug_sincos_compare(self, n, seed=0):

@@ -178,8 +178,9 @@ def generate_with_stats(params: GeneratorParams, *, device=None, shard: Shard | 
     model = params.resolve()
     _check_model_domain(model)
     eng = get_engine(device)
-    st = eng.generate(model, params.seed, VERTEX_ORDERS[params.vertex_order], shard)
-    indptr, indices = eng.copy_csr(np.int64, pinned=pinned)
+    with eng.lock:  # the result read back is this call's
+        st = eng.generate(model, params.seed, VERTEX_ORDERS[params.vertex_order], shard)
+        indptr, indices = eng.copy_csr(np.int64, pinned=pinned)
     graph = Graph(indptr=indptr, indices=indices)
     if params.long_range_fraction > 0.0:
         graph = add_long_range_edges(graph, params.long_range_fraction, params.seed)
@@ -213,8 +214,9 @@ def edges_from_coordinates(coords, radius, *, alpha=1.0, device=None, shard=None
     if n == 0:
         return Graph.from_edge_arrays(0, [], [])
     eng = get_engine(device)
-    eng.edges_from_coords(model, phi, rp, shard)
-    indptr, indices = eng.copy_csr(np.int64, pinned=pinned)
+    with eng.lock:
+        eng.edges_from_coords(model, phi, rp, shard)
+        indptr, indices = eng.copy_csr(np.int64, pinned=pinned)
     return Graph(indptr=indptr, indices=indices)
 
 
@@ -230,9 +232,10 @@ def generate_brute_force(coords, radius, *, device=None) -> Graph:
     if n == 0:
         return Graph.from_edge_arrays(0, [], [])
     eng = get_engine(device)
-    generate_brute_force.last_near_ties = eng.edges_brute_force(coords.phi, coords.r_poincare,
-                                                                float(radius))
-    indptr, indices = eng.copy_csr(np.int64)
+    with eng.lock:
+        generate_brute_force.last_near_ties = eng.edges_brute_force(coords.phi, coords.r_poincare,
+                                                                    float(radius))
+        indptr, indices = eng.copy_csr(np.int64)
     return Graph(indptr=indptr, indices=indices)
 
 

@@ -12,21 +12,23 @@ from paper_1501_03545_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "hrgen_b200.h")
+DEBUG_HEADER = os.path.join(ROOT, "include", "hrgen_b200_debug.h")
 
 
-def declared_functions():
-    text = open(HEADER).read()
+def declared_functions(path=HEADER):
+    text = open(path).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(hrg_[a-z_]+)\s*\(", text)))
 
 
 def test_header_and_binding_agree():
     assert set(declared_functions()) == set(_lib.EXPORTED)
+    assert set(declared_functions(DEBUG_HEADER)) == set(_lib.EXPORTED_DEBUG)
 
 
 def test_library_exports_every_declared_symbol():
     L = _lib.load()
-    for name in declared_functions():
+    for name in declared_functions() + declared_functions(DEBUG_HEADER):
         assert hasattr(L, name), name
 
 
