@@ -451,11 +451,14 @@ def run_ours(args):
                 got = np.column_stack((rows[keep], ix[keep]))
                 del rows, keep, ix
                 d = O.compare_edge_sets(got, pairs, phi, rp, model.R)
+                cls = O.classify_mismatches(d, phi, rp, consts["cosh_r_minus_1"])
                 parity = {"scope": "whole edge set", "ref": "oracle quadtree (hrgen "
                           "quadtree.py restated), libm trig = hrgen's arithmetic",
                           "m_gpu": d["m_got"], "m_ref": d["m_want"],
                           "mismatches": d["only_got"] + d["only_want"],
                           "max_rel_gap": d["max_gap"], "outside_band": d["outside_band"],
+                          "in_band": cls["band"], "ref_pruning_drops": cls["ref_drop"],
+                          "unexplained": cls["unexplained"],
                           "band": "|cosh d - cosh R| <= 1e-12 cosh R"}
                 del got, pairs
         except Exception as e:  # pragma: no cover

@@ -213,7 +213,7 @@ def compare_edge_sets(got, want, phi, rp, R, band=1e-12):
     n = int(max(got.max(initial=-1), want.max(initial=-1))) + 1
     if got.shape == want.shape and np.array_equal(got, want):
         return dict(m_got=len(got), m_want=len(want), only_got=0, only_want=0, max_gap=0.0,
-                    outside_band=0, pairs=np.empty((0, 2), np.int64))
+                    outside_band=0, pairs=np.empty((0, 2), np.int64), gaps=np.empty(0))
     kg = got[:, 0] * n + got[:, 1]   # both ascending (lexicographic order)
     kw = want[:, 0] * n + want[:, 1]
 
@@ -230,7 +230,47 @@ def compare_edge_sets(got, want, phi, rp, R, band=1e-12):
     gap = cosh_gap(pairs, phi, rp, R)
     return dict(m_got=len(got), m_want=len(want), only_got=int(only_g.size),
                 only_want=int(only_w.size), max_gap=float(gap.max(initial=0.0)),
-                outside_band=int(np.count_nonzero(gap > band)), pairs=pairs)
+                outside_band=int(np.count_nonzero(gap > band)), pairs=pairs, gaps=gap)
+
+
+RIM_ULPS = 2.0 ** -46   # 1 - r_p below this: a point within ~64 ulps of the disk's rim
+
+
+def classify_mismatches(d, phi, rp, a, band=1e-12):
+    """Sort the pairs of a compare_edge_sets result into
+      band      -- |cosh d - cosh R| <= band cosh R (the north star's exception);
+      ref_drop  -- present only in the GPU set, accepted by the reference's own
+                   leaf predicate (quadtree.py:611-613, circle of the smaller id;
+                   checked here by all-pairs rows), with an endpoint at the rim
+                   (1 - r_p < 2^-46): pairs hrgen's quadtree prunes although its
+                   predicate accepts them -- its leaf window (quadtree.py:573-590)
+                   and the predicate round differently where fp64 Poincare
+                   coordinates cannot resolve the hyperbolic distance;
+      unexplained -- everything else (a real disagreement).
+    Returns the counts."""
+    pairs = d["pairs"]
+    out = {"band": 0, "ref_drop": 0, "unexplained": 0}
+    if pairs.size == 0:
+        return out
+    n_got = d["only_got"]
+    got_only = pairs[:n_got]
+    gaps = d["gaps"]
+    inband = gaps <= band
+    out["band"] = int(inband.sum())
+    # GPU-only pairs outside the band: the reference predicate on all pairs
+    cand = got_only[~inband[:n_got]]
+    if cand.size:
+        q = np.unique(cand[:, 0])
+        ip, ix = rows_brute(phi, rp, a, q)
+        row = {int(v): ix[ip[k]:ip[k + 1]] for k, v in enumerate(q)}
+        for u, v in cand.tolist():
+            rim = max(rp[u], rp[v]) >= 1.0 - RIM_ULPS
+            if rim and np.isin(v, row[u]).item():
+                out["ref_drop"] += 1
+            else:
+                out["unexplained"] += 1
+    out["unexplained"] += int((~inband[n_got:]).sum())
+    return out
 
 
 def edge_hash(pairs):

@@ -380,10 +380,11 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sort_rows_smem<kLargeMax, 2>()));
   }
-  // range query: dense blocks (count pass + write pass, hrg_block.cuh; the
-  // default) or the per-query window walk (k_light + staging + compaction)
-  bool block = true;
-  if (const char* e = getenv("HRG_QUERY")) block = strcmp(e, "walk") != 0;
+  // range query: the per-query window walk (k_light + staging + compaction;
+  // the default) or dense blocks (HRG_QUERY=block: count pass + write pass
+  // straight into the CSR, hrg_block.cuh -- measured slower)
+  bool block = false;
+  if (const char* e = getenv("HRG_QUERY")) block = strcmp(e, "block") == 0;
   // segment slots per light query: the wide variant when most of the 32
   // bands hold points (expected >= 1 point per band, from the radial CDF
   // (cosh(alpha r) - 1) / (cosh(alpha R) - 1)), so light queries reach them all
@@ -1247,6 +1248,18 @@ hrg_status hrg_debug_sincos(hrg_context* c, int64_t n, const double* x, int mode
   b.release();
   return HRG_OK;
 }
+
+#ifdef HRG_BLOCK_PROFILE
+// experiments: per-band counters of the block query (reset after reading)
+hrg_status hrg_debug_block_profile(hrg_context* c, unsigned long long* out) {
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpyFromSymbol(out, g_bprof, sizeof(g_bprof)));
+  std::vector<unsigned long long> z(sizeof(g_bprof) / 8, 0ull);
+  CUDA_TRY(cudaMemcpyToSymbol(g_bprof, z.data(), sizeof(g_bprof)));
+  return HRG_OK;
+}
+#endif
 
 hrg_status hrg_synchronize(hrg_context* c) {
   if (!c) return fail(HRG_ERR_PARAMETER_DOMAIN, "ctx is NULL");

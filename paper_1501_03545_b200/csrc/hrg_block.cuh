@@ -41,13 +41,13 @@
 namespace hrg {
 
 #ifndef HRG_BLOCK_G
-#define HRG_BLOCK_G 32
+#define HRG_BLOCK_G 64
 #endif
 #ifndef HRG_BLOCK_HITCAP
 #define HRG_BLOCK_HITCAP 2048
 #endif
 #ifndef HRG_BLOCK_MINB_COUNT
-#define HRG_BLOCK_MINB_COUNT 6
+#define HRG_BLOCK_MINB_COUNT 8
 #endif
 #ifndef HRG_BLOCK_MINB_WRITE
 #define HRG_BLOCK_MINB_WRITE 4
@@ -56,6 +56,11 @@ namespace hrg {
 #define HRG_BLOCK_TILECAP 2048
 #endif
 
+#ifdef HRG_BLOCK_PROFILE
+// per band of the tile: [0] clock cycles, [1] tiles, [2] sub-tiles, [3] chunks,
+// [4] (query, chunk) iterations, [5] tests; [6] union rounds (experiments only)
+__device__ unsigned long long g_bprof[2][kMaxBands][8];
+#endif
 constexpr int kBlockThreads = 128;
 constexpr int kBlockG = HRG_BLOCK_G;        // union overhead target, records per sub-tile
 constexpr int kHitCap = HRG_BLOCK_HITCAP;   // T' * U bound: the write pass's row buffer per warp
@@ -92,7 +97,81 @@ __device__ __forceinline__ bool block_test(const QB& q, const QB& r) {
   const double x = lower ? q.px : r.px, y = lower ? q.py : r.py;
   const double cx = lower ? r.cx : q.cx, cy = lower ? r.cy : q.cy;
   const double rs = lower ? r.rsq : q.rsq;
-  return ref_pred(x, y, cx, cy, rs) && r.id != q.id;
+  // non-short-circuit: no branch (and no reconvergence around the ballot)
+  return ref_pred(x, y, cx, cy, rs) & (r.id != q.id);
+}
+
+// A sub-tile's union as the chunk loop needs it (per lane = band j): the
+// exclusive prefix of the band's union size, its A-part length and the
+// starts of both parts; U = the union's total size (warp-uniform).
+struct SubUnion {
+  int32_t excl, lenA, sA, sB, U;
+};
+
+// Record of flat union index c0 + lane (band = last lane j with excl_j <= i;
+// id -1 past the end).
+template <bool kSampleIds>
+__device__ __forceinline__ QB fetch_rec(const QueryArgs& A, const SubUnion& S, int32_t c0) {
+  const unsigned FULL = 0xffffffffu;
+  const int32_t i = c0 + (int32_t)(threadIdx.x & 31);
+  int o = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1)
+    if (__shfl_sync(FULL, S.excl, o + s) <= i) o += s;
+  const int32_t off = i - __shfl_sync(FULL, S.excl, o);
+  const int32_t la = __shfl_sync(FULL, S.lenA, o);
+  const int32_t sa = __shfl_sync(FULL, S.sA, o), sbb = __shfl_sync(FULL, S.sB, o);
+  QB r;
+  if (i < S.U) {
+    r = load_qb<kSampleIds>(A, off < la ? sa + off : sbb + (off - la));
+  } else {
+    r.px = r.py = r.cx = r.cy = r.rsq = 0.0;
+    r.id = -1;
+  }
+  return r;
+}
+
+// The T x U block of one sub-tile (queries q0 .. q0 + T - 1 of the tile):
+// kIn chunks of 32 records in flight per step, the T queries unrolled with
+// their hit counts in registers.  cnt (this lane's query) receives its
+// count; the write pass stores each query's hits at obase[oofs_q + k].
+template <int T, bool kSampleIds, bool kWrite>
+__device__ __forceinline__ void block_chunks(const QueryArgs& A, const SubUnion& S, const QB* qs,
+                                             int q0, int32_t& cnt, int32_t* obase, int64_t oofs) {
+  constexpr int kIn = T == 1 ? 4 : (T <= 4 ? 2 : 1);
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t cq[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) cq[t] = 0;
+  // T = 1: the query stays in registers
+  QB Q1;
+  if (T == 1) Q1 = qs[q0];
+  for (int32_t c0 = 0; c0 < S.U; c0 += 32 * kIn) {
+    QB r[kIn];
+#pragma unroll
+    for (int k = 0; k < kIn; ++k) r[k] = fetch_rec<kSampleIds>(A, S, c0 + 32 * k);
+#pragma unroll
+    for (int k = 0; k < kIn; ++k) {
+      if (c0 + 32 * k >= S.U) break;
+      const bool ok = r[k].id >= 0;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const QB Q = T == 1 ? Q1 : qs[q0 + t];
+        const bool hit = ok & block_test(Q, r[k]);
+        const unsigned m = __ballot_sync(FULL, hit);
+        if (kWrite) {
+          const int64_t at = __shfl_sync(FULL, oofs, q0 + t) + cq[t];
+          if (hit) obase[at + __popc(m & lt)] = r[k].id;
+        }
+        cq[t] += __popc(m);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t)
+    if (lane == q0 + t) cnt = cq[t];
 }
 
 template <bool kSampleIds, bool kWrite>
@@ -123,13 +202,12 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
     const int64_t ni = i < A.L ? max(0, sb[i].end - sb[i].start) : 0;
     const double t = tot > 0 ? (double)kBlockG * (double)ni / (double)tot : 1.0;
     int ts = 1;
-    while (ts < 32 && 2.0 * ts <= t) ts <<= 1;
+    while (ts < 16 && 2.0 * ts <= t) ts <<= 1;
     s_tsub[i] = ts;
   }
   __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
   QB* qs = s_q[threadIdx.x >> 5];
   int32_t* hb = s_hb[kWrite ? (threadIdx.x >> 5) : 0];
   unsigned long long* counter = A.tile_next + (kWrite ? 1 : 0);
@@ -137,6 +215,10 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
   for (int64_t tk = __shfl_sync(FULL, lane == 0 ? (int64_t)atomicAdd(counter, 1ull) : 0, 0);
        tk < A.ntiles;
        tk = __shfl_sync(FULL, lane == 0 ? (int64_t)atomicAdd(counter, 1ull) : 0, 0)) {
+#ifdef HRG_BLOCK_PROFILE
+    const long long clk0 = clock64();
+    unsigned long long pf_sub = 0, pf_chunks = 0, pf_iter = 0, pf_rounds = 0;
+#endif
     const uint64_t tv = __ldg(A.tiles + tk);
     if (tv == ~0ull) break;
     const int32_t v0 = (int32_t)(tv & 0xffffffffu);
@@ -178,7 +260,8 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
     int32_t cnt = 0;  // this lane's query: hits so far
     int q0 = 0;
     while (q0 < nq) {
-      int T = min(t0, nq - q0);
+      int T = t0;  // a power of two <= 16
+      while (T > nq - q0) T >>= 1;
       int32_t sA = 0, eA = 0, sB = 0, eB = 0, U = 0;
       for (;;) {
         const bool in = lane >= q0 && lane < q0 + T;
@@ -190,6 +273,9 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
           pmax = fmax(pmax, __shfl_xor_sync(FULL, pmax, o));
           rmin = fminf(rmin, __shfl_xor_sync(FULL, rmin, o));
         }
+#ifdef HRG_BLOCK_PROFILE
+        pf_rounds += 1;
+#endif
         if (T > 1 && pmax - pmin >= 0.5) { T >>= 1; continue; }
         sA = eA = sB = eB = 0;
         if (lane < A.L) {
@@ -219,6 +305,9 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
         continue;
       }
       if (lane == 0) tests += (unsigned long long)T * (unsigned long long)U;
+#ifdef HRG_BLOCK_PROFILE
+      pf_sub += 1; pf_chunks += (U + 31) / 32; pf_iter += (unsigned long long)((U + 31) / 32) * T;
+#endif
       const int32_t lenA = eA - sA, len = lenA + (eB - sB);
       int32_t incl = len;
 #pragma unroll
@@ -226,31 +315,13 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
         const int32_t y = __shfl_up_sync(FULL, incl, o);
         if (lane >= o) incl += y;
       }
-      const int32_t excl = incl - len;
-      for (int32_t c0 = 0; c0 < U; c0 += 32) {
-        // record of flat index i: band = last lane j with excl_j <= i
-        const int32_t i = c0 + lane;
-        int o = 0;
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1)
-          if (__shfl_sync(FULL, excl, o + s) <= i) o += s;
-        const int32_t off = i - __shfl_sync(FULL, excl, o);
-        const int32_t la = __shfl_sync(FULL, lenA, o);
-        const int32_t sa = __shfl_sync(FULL, sA, o), sbb = __shfl_sync(FULL, sB, o);
-        const bool ok = i < U;
-        QB r;
-        if (ok) r = load_qb<kSampleIds>(A, off < la ? sa + off : sbb + (off - la));
-        else { r.px = r.py = r.cx = r.cy = r.rsq = 0.0; r.id = -1; }
-        for (int q = q0; q < q0 + T; ++q) {
-          const QB Q = qs[q];
-          const bool hit = ok && block_test(Q, r);
-          const unsigned m = __ballot_sync(FULL, hit);
-          if (kWrite) {
-            const int64_t at = __shfl_sync(FULL, oofs, q) + __shfl_sync(FULL, cnt, q);
-            if (hit) obase[at + __popc(m & lt)] = r.id;
-          }
-          if (lane == q) cnt += __popc(m);
-        }
+      const SubUnion S{incl - len, lenA, sA, sB, U};
+      switch (T) {
+        case 1: block_chunks<1, kSampleIds, kWrite>(A, S, qs, q0, cnt, obase, oofs); break;
+        case 2: block_chunks<2, kSampleIds, kWrite>(A, S, qs, q0, cnt, obase, oofs); break;
+        case 4: block_chunks<4, kSampleIds, kWrite>(A, S, qs, q0, cnt, obase, oofs); break;
+        case 8: block_chunks<8, kSampleIds, kWrite>(A, S, qs, q0, cnt, obase, oofs); break;
+        default: block_chunks<16, kSampleIds, kWrite>(A, S, qs, q0, cnt, obase, oofs); break;
       }
       if (!kWrite && lane >= q0 && lane < q0 + T) {
         A.deg[row] = cnt;
@@ -258,6 +329,14 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
       }
       q0 += T;
     }
+#ifdef HRG_BLOCK_PROFILE
+    if (lane == 0 && bi >= 0) {
+      unsigned long long* P = g_bprof[kWrite ? 1 : 0][bi];
+      atomicAdd(P + 0, (unsigned long long)(clock64() - clk0));
+      atomicAdd(P + 1, 1ull); atomicAdd(P + 2, pf_sub); atomicAdd(P + 3, pf_chunks);
+      atomicAdd(P + 4, pf_iter); atomicAdd(P + 6, pf_rounds);
+    }
+#endif
     if (kWrite) {
       // the recomputed row must have the count pass's length (a mismatch
       // would be a bug: fail the generation loudly instead of writing it)

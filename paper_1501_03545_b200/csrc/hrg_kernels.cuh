@@ -611,20 +611,28 @@ __device__ __forceinline__ int32_t row_of(const QueryArgs& A, int32_t v) {
 __global__ void k_rowidx(const Band* __restrict__ bands, int L, const int32_t* __restrict__ ids,
                          int32_t* __restrict__ rowidx, int32_t* __restrict__ row_ids,
                          int64_t* __restrict__ nq) {
-  __shared__ int64_t base[kMaxBands + 1];
+  // base[j]: first row of band j (+inf past L, for the search)
+  __shared__ int64_t base[kMaxBands], s_total;
+  __shared__ int32_t qs0[kMaxBands];
   if (threadIdx.x == 0) {
     int64_t a = 0;
-    for (int j = 0; j < L; ++j) { base[j] = a; a += max(0, bands[j].qend - bands[j].qstart); }
-    base[L] = a;
+    for (int j = 0; j < kMaxBands; ++j) {
+      base[j] = j < L ? a : INT64_MAX;
+      qs0[j] = j < L ? bands[j].qstart : 0;
+      if (j < L) a += max(0, bands[j].qend - bands[j].qstart);
+    }
+    s_total = a;
     if (blockIdx.x == 0) *nq = a;
   }
   __syncthreads();
-  const int64_t total = base[L];
+  const int64_t total = s_total;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
-    int j = 0;
-    while (j + 1 < L && base[j + 1] <= k) ++j;
-    const int32_t pos = bands[j].qstart + (int32_t)(k - base[j]);
+    int j = 0;  // last band with base[j] <= k (binary search; bands past L are +inf)
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1)
+      if (base[j + st] <= k) j += st;
+    const int32_t pos = qs0[j] + (int32_t)(k - base[j]);
     rowidx[pos] = (int32_t)k;
     row_ids[k] = ids[pos];
   }
@@ -1112,10 +1120,12 @@ __device__ __forceinline__ void union_window(const QueryArgs& A, const Band& B, 
                                              float dlt_f, int32_t& sA, int32_t& eA,
                                              int32_t& sB, int32_t& eB) {
   RawWin r = raw_window(A, B, mid, dlt_f);
-  const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
-  const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
-  const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
-  finish_trim(A.keys, r, kA0, kA1, kB0);
+  if (HRG_TRIM_UNION) {
+    const uint64_t kA0 = (r.sA < r.eA && r.tlA) ? __ldg(A.keys + r.sA) : 0;
+    const uint64_t kA1 = (r.sA < r.eA && r.thA <= kQMask) ? __ldg(A.keys + r.eA - 1) : 0;
+    const uint64_t kB0 = (r.sB < r.eB && r.tlB) ? __ldg(A.keys + r.sB) : 0;
+    finish_trim(A.keys, r, kA0, kA1, kB0);
+  }
   if (r.sB < r.eB && r.sB < r.eA) {  // the window wraps onto itself: whole band
     r.sA = B.start; r.eA = B.end; r.sB = r.eB = 0;
   }

@@ -15,6 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from .engine import Shard, get_engine
+from .errors import ParameterDomainError
 from .generator import VERTEX_ORDERS, GeneratorParams, _check_model_domain, _stats
 from .graph import Graph
 
@@ -62,6 +63,12 @@ def generate_distributed(params: GeneratorParams, *, group=None, device=None, en
     import torch
     import torch.distributed as dist
 
+    if params.long_range_fraction > 0.0:
+        # hrgen adds long-range edges to the finished graph (generator.py:
+        # 228-229): a rank holds only its sector's rows, so it cannot draw them
+        raise ParameterDomainError(
+            "long_range_fraction > 0 needs the whole graph; generate it on one rank or add "
+            "the edges after gathering the rows (add_long_range_edges)")
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     model = params.resolve()

@@ -47,7 +47,9 @@ class GeneratorParams:
     """hrgen generator.py:51-106.  Exactly one of (avg_degree, radius) and
     one of (gamma, alpha).  Extra field: vertex_order ("sample": vertex i is
     the i-th draw, hrgen's labelling; "angular": ids in (band, angle) order,
-    an isomorphic relabelling whose CSR rows need no sort)."""
+    whose CSR rows need no sort -- hrgen's edge rule applied to those labels,
+    which decides a few borderline pairs differently from the sample-order
+    graph: 1601 of 1.6e8 at config 2, so it is not exactly a relabelling)."""
 
     n: int
     avg_degree: float | None = None
@@ -174,7 +176,11 @@ def _stats(model, st) -> GenerationStats:
 
 def generate_with_stats(params: GeneratorParams, *, device=None, shard: Shard | None = None,
                         pinned: bool = True):
-    """hrgen generator.py:190-239."""
+    """hrgen generator.py:190-239.  With `shard`, only that angular sector's
+    rows are emitted (multi-GPU; see distributed.py)."""
+    if shard is not None and shard.count > 1 and params.long_range_fraction > 0.0:
+        raise ParameterDomainError(
+            "long_range_fraction > 0 needs the whole graph, not one shard's rows")
     model = params.resolve()
     _check_model_domain(model)
     eng = get_engine(device)

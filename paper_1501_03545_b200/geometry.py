@@ -133,18 +133,3 @@ def model_constants(R: float, alpha: float):
         "two_over_alpha": 2.0 / alpha,
         "sinh_half_alpha_r": math.sinh(alpha * R / 2.0),
     }
-
-
-def circle_params_host(r_poincare, hyperbolic_radius):
-    """Host numpy form of the circle transform (hrgen geometry.py:141-157),
-    kept for API compatibility; the GPU evaluates the same expression per
-    vertex inside the index build."""
-    rh = np.asarray(r_poincare, dtype=np.float64)
-    a = 2.0 * np.sinh(np.asarray(hyperbolic_radius, dtype=np.float64) / 2.0) ** 2
-    b = (1.0 - rh) * (1.0 + rh)
-    denom = a * b + 2.0
-    center_r = 2.0 * rh / denom
-    disc = center_r**2 - (2.0 * rh**2 - a * b) / denom
-    if np.any(disc < 0.0):
-        raise AssertionError("negative discriminant in circle transform; inputs out of domain")
-    return center_r, np.sqrt(disc)

@@ -514,3 +514,17 @@ def test_staging_regrowth_after_small_graph():
     g2 = P.generate(p)
     check_csr(g1)
     assert np.array_equal(g1.indptr, g2.indptr) and np.array_equal(g1.indices, g2.indices)
+
+
+def test_reference_pruning_drop_fixture(oracle):
+    """On hrgen's coordinates where hrgen's quadtree drops a pair its own
+    predicate accepts (tests/golden/make_prune_golden.py), the GPU returns
+    the predicate's edge set: hrgen's edges plus exactly that rim pair."""
+    import os
+    z = np.load(os.path.join(gd.GOLDEN, "prune_drop.npz"))
+    coords = VertexCoordinates(phi=z["phi"], r_native=None, r_poincare=z["r_poincare"])
+    g = P.edges_from_coordinates(coords, float(z["R"]), alpha=float(z["alpha"]))
+    assert np.array_equal(g.edge_array(), z["allpairs_edges"])
+    d = oracle.compare_edge_sets(g.edge_array(), z["hrgen_edges"], z["phi"], z["r_poincare"],
+                                 float(z["R"]))
+    assert d["only_got"] == 1 and d["only_want"] == 0

@@ -168,3 +168,20 @@ def test_sampler_formula_matches_reference_expression(oracle):
     want = np.minimum(want, np.nextafter(R, 0.0))
     assert np.allclose(rn, want, rtol=4e-16, atol=0)
     assert np.all(rp < k["max_r"])
+
+
+def test_reference_pruning_drop_fixture(oracle):
+    """tests/golden/prune_drop.npz (made by running hrgen): hrgen's quadtree
+    drops exactly one pair that its own leaf predicate accepts, a pair with a
+    point 1 ulp below the rim; the oracle's all-pairs predicate finds it."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "prune_drop.npz"))
+    ref, allp = z["hrgen_edges"], z["allpairs_edges"]
+    assert len(allp) == len(ref) + 1
+    d = oracle.compare_edge_sets(allp, ref, z["phi"], z["r_poincare"], float(z["R"]))
+    assert d["only_got"] == 1 and d["only_want"] == 0
+    a = float(2.0 * np.sinh(np.asarray(float(z["R"])) / 2.0) ** 2)
+    cls = oracle.classify_mismatches(d, z["phi"], z["r_poincare"], a)
+    assert cls == {"band": 0, "ref_drop": 1, "unexplained": 0}
+    again = oracle.edges_brute(z["phi"], z["r_poincare"], a, oracle.TRIG_LIBM)
+    assert np.array_equal(again, allp)
