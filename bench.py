@@ -405,7 +405,7 @@ def run_ours(args):
     tq = med["t_light_ms"] + med["t_heavy_ms"]
     bytes_query = model.n * POINT_RECORD_B + n_q * 12 + (nnz_all / world) * 4
     achieved = bytes_query / (tq / 1e3) / 1e9
-    traffic = None
+    traffic, binding = None, None
     tpath = os.path.join(ROOT, "profiles", "query_write_traffic.json")
     if os.path.exists(tpath):
         try:
@@ -413,6 +413,9 @@ def run_ours(args):
                 tj = json.load(fh)
             if tj.get("config") == args.config and tj.get("n_gpus", 1) == world:
                 traffic = tj.get("dram_bytes_per_launch")
+                # the resource that does bind the kernel (neither HBM nor FP64):
+                # from the same committed ncu capture
+                binding = tj.get("binding")
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -420,7 +423,8 @@ def run_ours(args):
                 "kernel": "range query k_light + k_heavy (pair tests, hits to staging)",
                 "algorithmic_bytes_per_launch": bytes_query, "launch_ms": tq,
                 "fp64": {"pair_tests": cand_all / world, "flop_per_test": 6,
-                         "tflops": cand_all / world * 6 / (tq / 1e3) / 1e12}}
+                         "tflops": cand_all / world * 6 / (tq / 1e3) / 1e12},
+                "binding": binding}
 
     cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
