@@ -26,6 +26,7 @@ from .generator import (
     edges_from_coordinates,
     generate,
     generate_brute_force,
+    generate_with_coordinates,
     generate_with_stats,
     radial_inverse_cdf,
     sample_points,
@@ -50,7 +51,8 @@ __all__ = [
     "OutOfBoundsError", "ParameterDomainError", "Shard", "TRIG_CR", "TRIG_LIBM", "TWO_PI",
     "VertexCoordinates",
     "add_long_range_edges", "alpha_from_gamma", "edges_from_coordinates", "expected_avg_degree",
-    "generate", "generate_brute_force", "generate_with_stats", "get_engine", "model_constants",
+    "generate", "generate_brute_force", "generate_with_coordinates", "generate_with_stats",
+    "get_engine", "model_constants",
     "radial_inverse_cdf", "sample_points", "target_radius", "to_native_radius",
     "to_poincare_radius",
 ]

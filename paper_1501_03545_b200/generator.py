@@ -196,6 +196,24 @@ def generate_with_stats(params: GeneratorParams, *, device=None, shard: Shard | 
     return graph, stats
 
 
+def generate_with_coordinates(params: GeneratorParams, *, device=None, pinned: bool = True):
+    """The north star's "coordinates plus an edge list" in one call: the
+    Graph of generate() and the VertexCoordinates it was built on (vertex i
+    at index i; the same arrays sample_points returns for these parameters),
+    both read back from the one generation."""
+    model = params.resolve()
+    _check_model_domain(model)
+    eng = get_engine(device)
+    with eng.lock:
+        eng.generate(model, params.seed, VERTEX_ORDERS[params.vertex_order])
+        indptr, indices = eng.copy_csr(np.int64, pinned=pinned)
+        phi, rn, rp = eng.copy_coords()
+    graph = Graph(indptr=indptr, indices=indices)
+    if params.long_range_fraction > 0.0:
+        graph = add_long_range_edges(graph, params.long_range_fraction, params.seed)
+    return graph, VertexCoordinates(phi=phi, r_native=rn, r_poincare=rp)
+
+
 def generate(params: GeneratorParams, *, device=None) -> Graph:
     """hrgen generator.py:242-246."""
     graph, _ = generate_with_stats(params, device=device)
@@ -287,5 +305,6 @@ def add_long_range_edges(graph: Graph, fraction, seed) -> Graph:
 __all__ = [
     "DEFAULT_GENERATOR_CAPACITY", "GenerationStats", "GeneratorParams", "VertexCoordinates",
     "add_long_range_edges", "edges_from_coordinates", "generate", "generate_brute_force",
+    "generate_with_coordinates",
     "generate_with_stats", "radial_inverse_cdf", "sample_points", "TWO_PI",
 ]

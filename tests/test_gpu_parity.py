@@ -528,3 +528,18 @@ def test_reference_pruning_drop_fixture(oracle):
     d = oracle.compare_edge_sets(g.edge_array(), z["hrgen_edges"], z["phi"], z["r_poincare"],
                                  float(z["R"]))
     assert d["only_got"] == 1 and d["only_want"] == 0
+
+
+def test_generate_with_coordinates(oracle):
+    """Coordinates plus edge list from one generation: the coordinates are
+    sample_points' and the graph is the oracle's edge set on them."""
+    p = GeneratorParams(n=30_000, avg_degree=12.0, gamma=2.7, seed=21)
+    model = p.resolve()
+    g, co = P.generate_with_coordinates(p)
+    ref = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    assert np.array_equal(co.phi, ref.phi) and np.array_equal(co.r_poincare, ref.r_poincare)
+    assert np.array_equal(co.r_native, ref.r_native)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                    P.to_poincare_radius(model.R), 512, oracle.TRIG_LIBM)
+    assert g.m == m and np.array_equal(g.edge_array(), e)
