@@ -327,7 +327,10 @@ def run_ours(args):
         k2 = max(2, min(2 * args.steps, 8))
         n_, nnz_ = eng.sizes()
         streams = [torch.cuda.Stream(device=local) for _ in range(2)]
-        engines = [P.Engine(local, stream=s.cuda_stream) for s in streams]
+        # the timed engine is one of the two contexts (a third context's
+        # buffers would not fit beside two at n = 1e8)
+        eng.set_stream(streams[0].cuda_stream)
+        engines = [eng, P.Engine(local, stream=streams[1].cuda_stream)]
         bufs = [(torch.empty(n_ + 1, dtype=torch.int64, pin_memory=True).numpy(),
                  torch.empty(int(nnz_ * 1.01) + 1024, dtype=torch.int64, pin_memory=True).numpy())
                 for _ in range(2)]
@@ -391,6 +394,7 @@ def run_ours(args):
                       "of one graph overlaps the generation of the next); inputs are 5 "
                       "scalar parameters"}
         del engines
+        eng.set_stream(None)
 
     if rank != 0:
         if dist is not None:
