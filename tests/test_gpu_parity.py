@@ -316,11 +316,18 @@ def test_shards_partition_the_rows():
     (dict(n=100_000, radius=35.50799080982715, alpha=0.6, seed=4), 8),
     (dict(n=300_000, avg_degree=64.0, gamma=2.2, seed=4), 8),
 ], ids=["n5-x8", "n3000-x7", "R35.5-x8", "k64-g2.2-x8"])
-def test_shards_union_is_the_graph(kw, count):
+def test_shards_union_is_the_graph(oracle, kw, count):
     """Sharded sampling (each rank samples and indexes only the points its
-    sector can reach) reproduces the single-GPU graph row for row."""
+    sector can reach) reproduces the single-GPU graph row for row, and that
+    graph is the oracle's (hrgen's quadtree arithmetic) on its coordinates."""
     p = GeneratorParams(**kw)
     full = P.generate(p)
+    model = p.resolve()
+    co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                    P.to_poincare_radius(model.R), 512, oracle.TRIG_LIBM)
+    assert full.m == m and np.array_equal(full.edge_array(), e)
     acc = np.zeros(full.n, np.int64)
     for k in range(count):
         g, _ = P.generate_with_stats(p, shard=P.Shard(k, count))
