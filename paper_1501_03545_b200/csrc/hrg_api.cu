@@ -1171,68 +1171,89 @@ hrg_status hrg_result_device_ptrs(hrg_context* c, const double** phi, const doub
 
 namespace {
 
-// 8-byte ids into pageable HOST memory: the int32 ids cross PCIe (half the
-// bytes of int64) into pinned staging, chunk by chunk with all copies queued at once,
+// 8-byte ids into HOST memory: int32 ids cross PCIe (half the bytes of int64)
+// into pinned staging, chunk by chunk with all copies queued at once,
 // and the host threads widen each chunk into the caller's array as soon as
 // its copy has landed (every thread takes a slice of every chunk, so the
-// widening trails the copy by one chunk).  HRG_HOST_WIDEN=0 keeps the
-// device-side widening and the int64 copy.
+// widening trails the copy by one chunk).
 constexpr size_t kWidenChunk = (size_t)1 << 24;  // ids per staged chunk (64 MB)
+#ifndef HRG_PINNED_DEVICE_FRAC
+#define HRG_PINNED_DEVICE_FRAC 0.45
+#endif
+constexpr double kPinnedDeviceFrac = HRG_PINNED_DEVICE_FRAC;
 
 // Measured (config 2, 3.2e8 ids, 16 host cores): into PAGEABLE memory the
 // host widening takes 51 ms against 157 ms for the int64 copy (which stages
-// through the driver's bounce buffers); into PINNED memory the device
-// widening + one int64 DMA is faster (49 ms against 58 ms: host memory
-// bandwidth, not PCIe, then binds).  So: host widening for pageable
-// destinations only.
-bool host_widen_wanted(const hrg_context* c, const void* dst) {
-  if (const char* e = getenv("HRG_HOST_WIDEN")) return atoi(e) != 0;
-  if ((size_t)c->nnz < ((size_t)1 << 22)) return false;
+// through the driver's bounce buffers).  Into PINNED memory the PCIe link and
+// the host's memory bandwidth are both busy, so the ids are split: the first
+// fraction f is widened on the device and copied as int64, the rest crosses
+// as int32 and is widened by the host threads while the copies run (PCIe
+// bytes 4 (1 + f) per id, host widening (1 - f) of the ids; f balances the
+// two).  Measured (tools/e2e_ab.py, bench.py's two-context e2e): f = 1 (one
+// int64 copy) 53.0 ms/step, 0.6 48.4, 0.45 47.5, 0.35 48.5, 0 49.6 -- the
+// host's memory bandwidth, shared by the DMA and the widening, not PCIe,
+// limits the gain.  HRG_WIDEN_DEVICE_FRAC overrides f.
+double device_widen_frac(const hrg_context* c, const void* dst) {
+  if (const char* e = getenv("HRG_WIDEN_DEVICE_FRAC")) return std::min(1.0, std::max(0.0, atof(e)));
+  if ((size_t)c->nnz < ((size_t)1 << 22)) return 1.0;
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, dst) != cudaSuccess) {
     cudaGetLastError();  // clear the query's error
-    return true;
+    return 0.0;
   }
-  return at.type == cudaMemoryTypeUnregistered;
+  return at.type == cudaMemoryTypeUnregistered ? 0.0 : kPinnedDeviceFrac;
 }
 
-hrg_status copy_indices_host_widen(hrg_context* c, int64_t* dst) {
+// ids [0, first) widened on the device and copied as int64; ids [first, nnz)
+// copied as int32 in chunks and widened by the host threads as each lands.
+hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first) {
   const size_t nnz = (size_t)c->nnz;
   cudaStream_t st = c->stream;
-  if (c->h_stage_bytes < 4 * nnz) {
+  const size_t nh = nnz - first;
+  if (first > 0) {
+    CUDA_TRY(c->widen.ensure(8 * first));
+    ++c->launches, k_widen<<<blocks_for((int64_t)first), 256, 0, st>>>((int64_t)first, c->idx_final,
+                                                                       c->widen.as<int64_t>());
+  }
+  if (c->h_stage_bytes < 4 * nh) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     c->h_stage = nullptr;
     c->h_stage_bytes = 0;
-    CUDA_TRY(cudaMallocHost(&c->h_stage, 4 * nnz));
-    c->h_stage_bytes = 4 * nnz;
+    CUDA_TRY(cudaMallocHost(&c->h_stage, std::max<size_t>(4 * nh, 4)));
+    c->h_stage_bytes = std::max<size_t>(4 * nh, 4);
   }
-  const size_t nch = (nnz + kWidenChunk - 1) / kWidenChunk;
+  const size_t nch = (nh + kWidenChunk - 1) / kWidenChunk;
   while (c->h_ev.size() < nch) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
     c->h_ev.push_back(e);
   }
   for (size_t ch = 0; ch < nch; ++ch) {
-    const size_t a = ch * kWidenChunk, b = std::min(nnz, a + kWidenChunk);
-    CUDA_TRY(cudaMemcpyAsync(c->h_stage + a, c->idx_final + a, 4 * (b - a),
+    const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
+    CUDA_TRY(cudaMemcpyAsync(c->h_stage + a, c->idx_final + first + a, 4 * (b - a),
                              cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(c->h_ev[ch], st));
   }
+  if (first > 0)
+    CUDA_TRY(cudaMemcpyAsync(dst, c->widen.p, 8 * first, cudaMemcpyDeviceToHost, st));
   const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::atomic<int> err{0};
   auto work = [&](unsigned t) {
     for (size_t ch = 0; ch < nch; ++ch) {
       if (cudaEventSynchronize(c->h_ev[ch]) != cudaSuccess) { err = 1; return; }
-      const size_t a = ch * kWidenChunk, b = std::min(nnz, a + kWidenChunk);
+      const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
       const size_t lo = a + (b - a) * t / T, hi = a + (b - a) * (t + 1) / T;
       const int32_t* src = c->h_stage;
-      for (size_t i = lo; i < hi; ++i) dst[i] = src[i];
+      int64_t* out = dst + first;
+      for (size_t i = lo; i < hi; ++i) out[i] = src[i];
     }
   };
-  std::vector<std::thread> pool;
-  for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto& th : pool) th.join();
+  if (nch > 0) {
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < T; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+  }
   if (err) return fail(HRG_ERR_CUDA, "index copy failed");
   return HRG_OK;
 }
@@ -1263,8 +1284,9 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
   if (indices && c->nnz > 0) {
     if (index_bytes == 4) {
       CUDA_TRY(cudaMemcpyAsync(indices, c->idx_final, 4 * (size_t)c->nnz, k, st));
-    } else if (mem_kind == HRG_MEM_HOST && host_widen_wanted(c, indices)) {
-      hrg_status ws = copy_indices_host_widen(c, static_cast<int64_t*>(indices));
+    } else if (mem_kind == HRG_MEM_HOST && device_widen_frac(c, indices) < 1.0) {
+      const size_t first = (size_t)(device_widen_frac(c, indices) * (double)c->nnz);
+      hrg_status ws = copy_indices_split(c, static_cast<int64_t*>(indices), first);
       if (ws != HRG_OK) return ws;
     } else {
       // widen on the device in one pass, then one copy: the copy engine then
