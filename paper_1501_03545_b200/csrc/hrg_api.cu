@@ -436,7 +436,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   int64_t nnz = 0, total_chunks = 0;
   for (int attempt = 0; attempt < 3; ++attempt) {
     const int64_t cap = c->stage_cap;  // also bounds hits, chunks, rows to sort
-    CUDA_TRY(c->stage.ensure(4 * (size_t)cap));
+    CUDA_TRY(c->stage.ensure(4 * (size_t)cap + 64));  // + slack: the compaction's TMA copies
+                                                       // round up to 16-byte boundaries
     A.stage = c->stage.as<int32_t>();
     A.stage_cap = cap;
     const int64_t hcap = np + 1;                     // deferred queries

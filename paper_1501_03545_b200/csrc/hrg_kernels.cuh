@@ -1821,6 +1821,52 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) signalled on an mbarrier.
+// HRG_COMPACT_TMA=1 stages each compaction group with one bulk copy instead
+// of per-lane cp.async: correct (parity suite) but measured 1.7% slower
+// (k_compact_light 1.492 -> 1.518 ms at config 2: one serialised bulk copy
+// per group against 32 lanes' copies in flight), so off by default.
+#ifndef HRG_COMPACT_TMA
+#define HRG_COMPACT_TMA 0
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// generic-proxy accesses of this thread's shared memory before async-proxy
+// (TMA) writes into it
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Compaction of light rows.  A warp owns the same 32 consecutive queries as
 // in k_light, whose hits k_light left back to back in the staging buffer,
 // row after row in candidate order.  With angular ids and no deferred query
@@ -1835,11 +1881,21 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
     QueryArgs A, const int64_t* __restrict__ rowptr, int32_t* __restrict__ idx, SortJobs J) {
   if (*A.overflow) return;  // void pass, re-run by the host
   __shared__ Band sb[kMaxBands];
-  __shared__ int32_t buf[kCompactThreads / 32][kTileHits];
+  // per warp: the group buffer (+ 8 ids: a TMA copy starts at the 16-byte
+  // boundary below the group's first hit) and its mbarrier
+  __shared__ __align__(16) int32_t buf[kCompactThreads / 32][kTileHits + 8];
+  __shared__ __align__(8) uint64_t s_bar[kCompactThreads / 32];
   load_bands(A, sb);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  int32_t* sm = buf[threadIdx.x >> 5];
+  int32_t* const smraw = buf[threadIdx.x >> 5];
+  uint64_t* const bar = s_bar + (threadIdx.x >> 5);
+  unsigned bar_phase = 0;
+  if (HRG_COMPACT_TMA && lane == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // The per-row loads of a tile (its entry in the tile table, then heavy
@@ -1940,10 +1996,32 @@ __global__ void __launch_bounds__(kCompactThreads, HRG_COMPACT_MINB) k_compact_l
         const int l1 = 32 - __clz(fit);  // hits are non-decreasing: fit = lanes [l0, l1)
         const int32_t G = __shfl_sync(FULL, hi, l1 - 1) - start;
         const bool ing = lane >= l0 && lane < l1;
-        // asynchronous copies (no registers held): the whole group in flight
         const int32_t* gsrc = A.stage + base + start;
-        for (int32_t i = lane; i < G; i += 32) cp_async4(sm + i, gsrc + i);
-        cp_async_wait_all();
+        int32_t* sm = smraw;
+        if (HRG_COMPACT_TMA) {
+          // one 1-D TMA bulk copy of the group's staging range, widened to
+          // 16-byte boundaries (the staging buffer has 64 bytes of slack);
+          // the group's first hit sits sh ids into the buffer
+          const uintptr_t g0 = (uintptr_t)gsrc & ~(uintptr_t)15;
+          const int sh = (int)(((uintptr_t)gsrc - g0) >> 2);
+          const unsigned bytes =
+              (unsigned)((((uintptr_t)(gsrc + G) + 15) & ~(uintptr_t)15) - g0);
+          sm = smraw + sh;
+          __syncwarp();  // the previous group's reads and in-place sorts are done
+          if (G > 0) {
+            if (lane == 0) {
+              fence_proxy_async_smem();
+              mbar_expect_tx(bar, bytes);
+              bulk_g2s(smraw, (const void*)g0, bytes, bar);
+            }
+            mbar_wait(bar, bar_phase);
+            bar_phase ^= 1u;
+          }
+        } else {
+          // asynchronous copies (no registers held): the whole group in flight
+          for (int32_t i = lane; i < G; i += 32) cp_async4(sm + i, gsrc + i);
+          cp_async_wait_all();
+        }
         s_off[threadIdx.x] = hexcl - start;
         __syncwarp();
         if (kSampleIds) {
