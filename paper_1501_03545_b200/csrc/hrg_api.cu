@@ -86,7 +86,7 @@ struct hrg_context {
   // index
   Buf bands, dir, dir_total, bad, dir_gaps, band_pmin;
   // CSR
-  Buf deg, rowptr, idx, idx2, cand, rowidx, row_ids, rowptr_c, nq_buf;
+  Buf deg, rowptr, idx, cand, rowidx, row_ids, rowptr_c, nq_buf;
   bool compact_result = false;  // sharded: rows in sector-position order (expanded on request)
   int64_t nq = 0;
   Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep, sh_gid;
@@ -550,7 +550,9 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       // rows by length: a warp (<= kWarpBucketMax), a 256-thread block
       // (<= kBucketMax), a 1024-thread block (<= kLargeMax); giant (hub) rows
       // are first split by value into sub-buckets through the scratch array
-      CUDA_TRY(c->idx2.ensure(4 * (size_t)cap));
+      // scratch of the giant-row split: the staging buffer, dead once the
+      // compaction has run (saves a cap-sized buffer: 8 GB at n = 1e8)
+      int32_t* scratch = c->stage.as<int32_t>();
       const RowList none{nullptr, nullptr, nullptr};
       const unsigned sm = (unsigned)c->sm_count;
       // the length classes are independent (rows were queued straight into
@@ -569,9 +571,9 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       ++c->launches, k_giant_plan<<<1, 1024, 0, s2>>>(G);
       ++c->launches, k_giant_hist<<<2 * sm, 1024, 0, s2>>>(idx, G, n);
       ++c->launches, k_giant_scan<<<sm, 1024, 0, s2>>>(G);
-      ++c->launches, k_giant_scatter<<<2 * sm, 1024, 0, s2>>>(idx, c->idx2.as<int32_t>(), G, n);
+      ++c->launches, k_giant_scatter<<<2 * sm, 1024, 0, s2>>>(idx, scratch, G, n);
       ++c->launches, k_sort_rows<1024, kLargeMax, 2><<<sm, 1024, sort_rows_smem<kLargeMax, 2>(), s2>>>(
-          c->idx2.as<int32_t>(), idx, G.sub, none);
+          scratch, idx, G.sub, none);
       CUDA_TRY(cudaEventRecord(c->join[0], s1));
       CUDA_TRY(cudaEventRecord(c->join[1], s2));
       CUDA_TRY(cudaStreamWaitEvent(st, c->join[0], 0));
@@ -846,10 +848,12 @@ hrg_status expand_rows(hrg_context* c) {
                                                 c->row_ids.as<int32_t>(), c->deg.as<int32_t>());
   hrg_status s = scan_i32_to_i64(c, c->deg.as<int32_t>(), c->rowptr.as<int64_t>(), n);
   if (s != HRG_OK) return s;
-  // the compact rows are in idx (the compaction's output); idx2 is scratch
-  // once the row sorts are done
-  CUDA_TRY(c->idx2.ensure(4 * (size_t)std::max<int64_t>(c->nnz, 1)));
-  int32_t* out = c->idx2.as<int32_t>();
+  // the compact rows are in idx (the compaction's output); the staging
+  // buffer (>= nnz ids: every hit had a staging slot) is dead by now and
+  // takes the expanded rows
+  if (c->stage.bytes < 4 * (size_t)std::max<int64_t>(c->nnz, 1))
+    return fail(HRG_ERR_INTERNAL, "staging smaller than the result");
+  int32_t* out = c->stage.as<int32_t>();
   ++c->launches, k_expand_rows<<<8 * c->sm_count, 256, 0, st>>>(c->nq, c->rowptr_c.as<int64_t>(),
                                                  c->row_ids.as<int32_t>(), c->idx_final,
                                                  c->rowptr.as<int64_t>(), out);
@@ -914,7 +918,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
                  &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps, &c->band_pmin,
-                 &c->deg, &c->rowptr, &c->idx, &c->idx2, &c->cand, &c->rowidx, &c->row_ids, &c->rowptr_c, &c->nq_buf, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
+                 &c->deg, &c->rowptr, &c->idx, &c->cand, &c->rowidx, &c->row_ids, &c->rowptr_c, &c->nq_buf, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})
     b->release();
   if (c->h_rb) cudaFreeHost(c->h_rb);
