@@ -47,9 +47,6 @@ namespace hrg {
 #ifndef HRG_SMALL_SLOTS
 #define HRG_SMALL_SLOTS 64
 #endif
-#ifndef HRG_TRIM
-#define HRG_TRIM 0
-#endif
 #ifndef HRG_TRIM_UNION
 #define HRG_TRIM_UNION 1
 #endif
@@ -298,6 +295,7 @@ struct Recs {
 struct QRec {          // query-side extras, per sorted position
   double* phi;
   float* rf;           // a lower bound of the hyperbolic radius 2*atanh(r)
+  float* invd;         // an upper bound of 1 / D, D = a (1 - r)(1 + r) + 2 (see walk_test)
 };
 
 // Gather into (band, angle) order and precompute every per-point quantity the
@@ -359,12 +357,18 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
   circle_params(r, a, &cr, &rad);
   const double px = __dmul_rn(r, cs), py = __dmul_rn(r, sn);
   const double cx = __dmul_rn(cr, cs), cy = __dmul_rn(cr, sn), rsq = __dmul_rn(rad, rad);
+  rec.pt[p] = make_double2(px, py);
+  {
+    // 1 / D rounded up (float) with 2^-18 of slack: D = a b + 2 errs by a few
+    // ulps here, the walk's margin only needs an upper bound
+    const double D = a * ((1.0 - r) * (1.0 + r)) + 2.0;
+    q.invd[p] = __double2float_ru(1.0 / D) * (1.0f + 0x1p-18f);
+  }
   if (kSampleIds) {
     Rec R;
     R.px = px; R.py = py; R.cx = cx; R.cy = cy; R.rsq = rsq; R.id = id; R.pad = 0;
     rec.rec[p] = R;
   } else {
-    rec.pt[p] = make_double2(px, py);
     Circ ci;
     ci.cx = cx; ci.cy = cy; ci.rsq = rsq; ci.pad = 0.0;
     rec.circ[p] = ci;
@@ -567,9 +571,11 @@ struct QueryArgs {
   const int32_t* dir;
   const uint64_t* keys;      // sorted (band << 53 | angular key)
   const float* wtab;         // window half-width per (query-radius row, band); >= pi: whole band
+  const uint32_t* wtab_q;    // the same in 2^-32 turns (window_units)
   int wrows;
   int L;
   double C;                  // 2^53 / (2 pi)
+  double a;                  // 2 sinh^2(R/2) = cosh R - 1 (geometry.py:149)
   // staging: every light query owns one slot per candidate (hit id or -1);
   // a heavy query's slice holds its chunks' compacted hits at chunk * kChunk
   int32_t* stage;
@@ -710,10 +716,26 @@ __device__ __forceinline__ double poincare_halfwidth(double a, double e, double 
   return d >= pi ? 4.0 : d;
 }
 
+// The same half-width in units of 2^-32 of a turn, rounded up, for the
+// per-query windows' integer arithmetic on the top 32 bits q32 of the 53-bit
+// angular keys.  qkey floors a rounded product, so a point within dlt of the
+// query's angle -- and every key in [qkey(phi - dlt), qkey(phi + dlt)], the
+// fp64 window of the union / heavy path -- lies within dlt * C + 5 of the
+// query's key; q32 * 2^21 is up to 2^21 - 1 below that key, and
+// dq = floor(dlt * 2^32 / 2 pi) + 3 covers both: dq * 2^21 >= dlt * C + 2^22.
+constexpr uint32_t kWinWhole = 0xffffffffu, kWinEmpty = 0xfffffffeu;
+__device__ __forceinline__ uint32_t window_units(float dlt) {
+  if (dlt < 0.0f) return kWinEmpty;
+  if (dlt >= 3.14159f) return kWinWhole;
+  const double u = floor((double)dlt * (4294967296.0 / kTwoPi)) + 3.0;
+  return u >= 2147483648.0 ? kWinWhole : (uint32_t)u;
+}
+
 // Row s covers query (hyperbolic) radii [s*kRowStep, (s+1)*kRowStep); entry
 // < 0: no vertex of the band can be a neighbour; >= pi: the whole band.
 __global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, double a,
-                               double E, float* __restrict__ wtab) {
+                               double E, float* __restrict__ wtab,
+                               uint32_t* __restrict__ wtab_q = nullptr) {
   const int s = blockIdx.x, j = threadIdx.x;
   if (s >= rows || j >= L) return;
   const Band B = bands[j];
@@ -732,6 +754,7 @@ __global__ void k_window_table(const Band* __restrict__ bands, int L, int rows, 
     out = d < 0.0 ? -1.0f : (d >= 3.14159 ? 4.0f : __double2float_ru(d * 1.01));
   }
   wtab[s * L + j] = out;
+  if (wtab_q) wtab_q[s * L + j] = window_units(out);
 }
 
 // Sharded runs: the angular range of each band that any query of this
@@ -1135,7 +1158,6 @@ __device__ __forceinline__ void union_window(const QueryArgs& A, const Band& B, 
 }
 
 constexpr int kBandGroup = HRG_BAND_GROUP;    // bands resolved together (loads in flight)
-constexpr bool kTrim = HRG_TRIM;              // exact key trim of per-query windows
 constexpr bool kTrimUnion = HRG_TRIM_UNION;   // ... and of the tile's union windows
 constexpr int kUnionSmall = HRG_UNION_SMALL;  // union windows this small are shared by the tile
 constexpr int kShareSlack = HRG_SHARE_SLACK;  // (experiment) union shared if it exceeds the
@@ -1187,7 +1209,29 @@ __device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, i
 
 constexpr int kWalkUnroll = HRG_WALK_UNROLL;  // walk steps whose loads are in flight together
 constexpr int kFirstSeg = 1 << 30;            // flat entry: the query's first segment
-constexpr int kFlatMask = (1 << 30) - 1;      // flat entry: flat index << 5 | lane
+constexpr int kFlatMask = (1 << 21) - 1;      // flat entry: flat index << 5 | lane
+constexpr int kFlatBandShift = 21;            // ... | band << 21 (5 bits)
+static_assert(kLightMax * 32 <= (1 << 16), "a tile's flat candidate index must fit 16 bits");
+
+// The walk's pair test with a fixed orientation.  hrgen decides {v, w} with the
+// circle of the smaller id (generator.py:182-187).  The walk always evaluates
+// pred(v -> w): S = |P_w - C_v|^2 in ref_pred's own operation order against
+// rad_v^2, so a candidate costs one 16 B point (+ its id) instead of the 48 B
+// record.  For id_v < id_w that is hrgen's decision itself.  For id_w < id_v
+// hrgen evaluates pred(w -> v); with g_x = F / D_x the exact value of
+// orientation x (see "window table" above) and every fp64 evaluation within
+// e = 2^-45 of it, |S - rad_v^2| > e (1 + D_w / D_v) implies both evaluations
+// have the sign of F; only inside that margin (D_w bounded by the band's
+// innermost point) is the other orientation evaluated from w's full record.
+struct __align__(16) QHot {   // per query, shared memory: the walk's operands
+  double cx, cy, rsq;
+  float invd;                 // >= 1 / D_v
+  int32_t idv;                // vertex id (sample order) or position (angular)
+};
+struct __align__(16) QCold {  // per query: its point, for the other orientation
+  double px, py;
+};
+constexpr float kPredErrF = 0x1.000008p-45f;  // e, rounded up
 
 // Per-lane segment slots (kCap + 1 stride, padded against bank conflicts).
 // Two variants: kSegCap slots at 5 blocks/SM, and kSegCapWide slots at 4
@@ -1212,12 +1256,25 @@ template <int kCap>
 struct LightSmem {
   static constexpr int kStride = kCap + 1;
   int2 flat[kLightThreads / 32][32 * kStride];  // per warp: the tile's band segments
-  QFull q[kLightThreads];
+  QHot qh[kLightThreads];
+  QCold qc[kLightThreads];
   int32_t hits[kLightThreads];
+  float dband[kMaxBands];  // e * D of each band's innermost point, rounded up
 };
 
-template <int kCap>
-__device__ __forceinline__ const QFull& f_of(const LightSmem<kCap>& sm, int q) { return sm.q[q]; }
+// w's circle (c_x, c_y, rad^2), for pred(w -> v): the walk's margin case
+template <bool kSampleIds>
+__device__ __forceinline__ void load_other(const Recs& R, int32_t w, double2& cxy, double& rsq) {
+  if (kSampleIds) {
+    const Rec* r = R.rec + w;
+    cxy = __ldg(reinterpret_cast<const double2*>(&r->cx));
+    rsq = __ldg(&r->rsq);
+  } else {
+    const Circ* c = R.circ + w;
+    cxy = __ldg(reinterpret_cast<const double2*>(&c->cx));
+    rsq = __ldg(&c->rsq);
+  }
+}
 
 template <int kCap>
 constexpr size_t light_smem() { return sizeof(LightSmem<kCap>); }
@@ -1231,6 +1288,16 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
   __shared__ Band sb[kMaxBands];
   __shared__ LightSmem<kCap> sm;  // static: compile-time shared addresses
   load_bands(A, sb);
+  if (threadIdx.x < kMaxBands) {
+    const Band B = sb[threadIdx.x];
+    float d = 0.0f;
+    if (threadIdx.x < A.L && B.end > B.start) {
+      const double D = A.a * ((1.0 - B.pmin) * (1.0 + B.pmin)) + 2.0;
+      d = __double2float_ru(0x1p-45 * D) * (1.0f + 0x1p-18f);
+    }
+    sm.dband[threadIdx.x] = d;
+  }
+  __syncthreads();
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
@@ -1255,6 +1322,8 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     bool ovf = false;
     const double phi = active ? A.q.phi[v] : 0.0;
     const float rvq = active ? A.q.rf[v] : 3.0e38f;
+    const uint32_t q32 = (uint32_t)(qkey(phi, A.C) >> (kQBits - 32));
+    const uint32_t* wrowq = A.wtab_q + (wtab_row(A, rvq) - A.wtab);
     // ---- tile-level union windows (lane = band): the 32 queries are
     // angular neighbours, so in bands where their windows are wide relative
     // to the tile's angular span one resolution serves all of them.  Bands
@@ -1308,22 +1377,26 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
       }
       if (!active) continue;
       {
-        const float* wrow = wtab_row(A, rvq);
+        // per-query windows at directory granularity, in integer arithmetic
+        // on the top 32 bits of the query's angular key: [q - dq, q + dq]
+        // wraps mod 2^32 like the angle; two directory reads per band
         RawWin w[kBandGroup];
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
           const int j = jg + u;
-          if (j < A.L && !((cheap >> j) & 1u)) w[u] = raw_window(A, sb[j], phi, __ldg(wrow + j));
-          else w[u] = RawWin{0, 0, 0, 0, 0, kQMask + 1, 0};
-        }
-        uint64_t kA0[kBandGroup], kA1[kBandGroup], kB0[kBandGroup];
-#pragma unroll
-        for (int u = 0; u < kBandGroup; ++u) {
-          if (kTrim) {
-            kA0[u] = (w[u].sA < w[u].eA && w[u].tlA) ? __ldg(A.keys + w[u].sA) : 0;
-            kA1[u] = (w[u].sA < w[u].eA && w[u].thA <= kQMask) ? __ldg(A.keys + w[u].eA - 1) : 0;
-            kB0[u] = (w[u].sB < w[u].eB && w[u].tlB) ? __ldg(A.keys + w[u].sB) : 0;
-          }
+          w[u] = RawWin{0, 0, 0, 0, 0, kQMask + 1, 0};
+          if (j >= A.L || ((cheap >> j) & 1u)) continue;
+          const uint32_t dq = __ldg(wrowq + j);
+          const int32_t bs = sb[j].start, be = sb[j].end;
+          if (dq == kWinEmpty || be <= bs) continue;
+          if (dq == kWinWhole) { w[u].sA = bs; w[u].eA = be; continue; }
+          const uint32_t ql = q32 - dq, qh = q32 + dq;
+          const int sh = sb[j].shift - (kQBits - 32);
+          const int32_t* d = A.dir + sb[j].dir_base;
+          const int32_t lo = __ldg(d + (sh < 32 ? ql >> sh : 0u));
+          const int32_t hi = __ldg(d + (sh < 32 ? qh >> sh : 0u) + 1);
+          if (q32 < dq || qh < q32) { w[u].sA = bs; w[u].eA = hi; w[u].sB = lo; w[u].eB = be; }
+          else { w[u].sA = lo; w[u].eA = hi; }
         }
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
@@ -1333,17 +1406,18 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
           if ((cheap >> j) & 1u) {
             r.sA = gA[u]; r.eA = gAe[u]; r.sB = gB[u]; r.eB = gBe[u];
           } else {
-            if (kTrim) finish_trim(A.keys, r, kA0[u], kA1[u], kB0[u]);
             if (r.sB < r.eB && r.sB < r.eA) {  // window wraps onto itself: whole band
               r.sA = sb[j].start; r.eA = sb[j].end; r.sB = r.eB = 0;
             }
           }
           if (r.eA > r.sA) {
-            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sA, c); else ovf = true;
+            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sA, (c & 0xffff) | (j << 16));
+            else ovf = true;
             c += r.eA - r.sA;
           }
           if (r.eB > r.sB) {
-            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sB, c); else ovf = true;
+            if (nseg < kSegCap) fl_own[nseg++] = make_int2(r.sB, (c & 0xffff) | (j << 16));
+            else ovf = true;
             c += r.eB - r.sB;
           }
         }
@@ -1384,7 +1458,15 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     // lane).  Rounds run over destinations; every entry moves down (dest <=
     // source), so a round's writes never hit a source still to be read.
     int2* fl = sm.flat[tid >> 5];
-    if (light) sm.q[tid] = load_query<kSampleIds>(A, v);
+    if (light) {
+      const QFull f = load_query<kSampleIds>(A, v);
+      QHot h;
+      h.cx = f.cx; h.cy = f.cy; h.rsq = f.rsq; h.invd = A.q.invd[v]; h.idv = f.idv;
+      sm.qh[tid] = h;
+      QCold k;
+      k.px = f.px; k.py = f.py;
+      sm.qc[tid] = k;
+    }
     {
       const int32_t sb = sincl - nsl;
       for (int e0 = 0; e0 < S; e0 += 32) {
@@ -1398,7 +1480,9 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         int2 g = make_int2(0, 0);
         if (e < S) g = fl[l * kSegStride + k];
         __syncwarp();
-        if (e < S) fl[e] = make_int2(g.x, (k == 0 ? kFirstSeg : 0) | ((own_ex + g.y) << 5) | l);
+        if (e < S)
+          fl[e] = make_int2(g.x, (k == 0 ? kFirstSeg : 0) | ((g.y >> 16) << kFlatBandShift) |
+                                     ((own_ex + (g.y & 0xffff)) << 5) | l);
         __syncwarp();
       }
     }
@@ -1427,26 +1511,53 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
           s0 += __popc(mask);
           const int2 e = fl[my];
           const int32_t off = ib + lane - ((e.y & kFlatMask) >> 5);
-          qv[u] = e.y & 31;
-          qs[u] = off == 0 && (e.y & kFirstSeg);  // first candidate of its query
+          // query lane | band << 5 | first candidate of its query << 10
+          qv[u] = (e.y & 31) | (((e.y >> kFlatBandShift) & 31) << 5);
+          qs[u] = off == 0 && (e.y & kFirstSeg);
           wv[u] = e.x + off;
         }
-        LoadedCand r[kWalkUnroll];
+        double2 pt[kWalkUnroll];
+        int32_t idw[kWalkUnroll];
 #pragma unroll
         for (int u = 0; u < kWalkUnroll; ++u)
-          if (i0 + 32 * u + lane < T)
-            r[u] = load_walk_cand<kSampleIds>(A, sm.q[wb + qv[u]].pos, wv[u]);
+          if (i0 + 32 * u + lane < T) {
+            pt[u] = __ldg(A.rec.pt + wv[u]);
+            idw[u] = kSampleIds ? __ldg(A.rec.ids + wv[u]) : wv[u];
+          }
+        bool hit[kWalkUnroll], unc[kWalkUnroll];
+#pragma unroll
+        for (int u = 0; u < kWalkUnroll; ++u) {
+          hit[u] = unc[u] = false;
+          if (i0 + 32 * u + lane < T) {
+            const QHot f = sm.qh[wb + (qv[u] & 31)];
+            const double dx = __dsub_rn(pt[u].x, f.cx), dy = __dsub_rn(pt[u].y, f.cy);
+            const double s2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+            hit[u] = s2 < f.rsq && idw[u] != f.idv;  // quadtree.py:611-613 with v's circle
+            const float g = fabsf(__double2float_rn(__dsub_rn(s2, f.rsq)));
+            unc[u] = idw[u] < f.idv && g <= fmaf(sm.dband[qv[u] >> 5], f.invd, kPredErrF);
+          }
+        }
+        // margin cases (rare): w's circle decides.  Their loads are issued
+        // together and waited for once per group of steps.
+        double2 oc[kWalkUnroll];
+        double orsq[kWalkUnroll];
+#pragma unroll
+        for (int u = 0; u < kWalkUnroll; ++u)
+          if (unc[u]) load_other<kSampleIds>(A.rec, wv[u], oc[u], orsq[u]);
+#pragma unroll
+        for (int u = 0; u < kWalkUnroll; ++u)
+          if (unc[u]) {
+            const QCold k = sm.qc[wb + (qv[u] & 31)];
+            hit[u] = ref_pred(k.px, k.py, oc[u].x, oc[u].y, orsq[u]);
+          }
 #pragma unroll
         for (int u = 0; u < kWalkUnroll; ++u) {
           const int32_t i = i0 + 32 * u + lane;
-          bool hit = false;
-          int32_t id = 0;
-          if (i < T) hit = walk_test<kSampleIds>(f_of(sm, wb + qv[u]), r[u], wv[u], id);
           // hits only, compacted: the tile's rows end up back to back
-          const unsigned hm = __ballot_sync(FULL, hit);
+          const unsigned hm = __ballot_sync(FULL, hit[u]);
           const int32_t at = pre + __popc(hm & ((1u << lane) - 1u));
-          if (hit) out[at] = id;
-          if (qs[u] && i < T) sm.hits[wb + qv[u]] = at;
+          if (hit[u]) out[at] = idw[u];
+          if (qs[u] && i < T) sm.hits[wb + (qv[u] & 31)] = at;
           pre += __popc(hm);
         }
       }

@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: exp/ab_run.sh out.jsonl variant...   (env N K G SEED ORDER pass through)
+# usage: tools/ab_run.sh out.jsonl variant...   (env N K G SEED ORDER pass through)
 out=$1; shift
 for v in "$@"; do
   if [ "$v" = "default" ]; then lib=""; else lib="exp/lib_$v.so"; fi
