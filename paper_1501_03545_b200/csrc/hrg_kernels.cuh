@@ -42,7 +42,7 @@ namespace hrg {
 #define HRG_WALK_UNROLL 3
 #endif
 #ifndef HRG_BAND_GROUP
-#define HRG_BAND_GROUP 2
+#define HRG_BAND_GROUP 1
 #endif
 #ifndef HRG_SMALL_SLOTS
 #define HRG_SMALL_SLOTS 64
@@ -59,6 +59,9 @@ namespace hrg {
 #ifndef HRG_UNION_SMALL
 #define HRG_UNION_SMALL 2
 #endif
+#ifndef HRG_DENSE_MAX
+#define HRG_DENSE_MAX 8
+#endif
 #ifndef HRG_MID_SHIFT
 #define HRG_MID_SHIFT -1
 #endif
@@ -69,7 +72,7 @@ namespace hrg {
 #define HRG_COMPACT_MINB 5
 #endif
 #ifndef HRG_SEGCAP
-#define HRG_SEGCAP 28
+#define HRG_SEGCAP 20
 #endif
 #ifndef HRG_LIGHT_MAX
 #define HRG_LIGHT_MAX 2048
@@ -93,7 +96,7 @@ namespace hrg {
 #define HRG_HEAVY_BATCH 4
 #endif
 #ifndef HRG_LIGHT_MINBLOCKS
-#define HRG_LIGHT_MINBLOCKS 5
+#define HRG_LIGHT_MINBLOCKS 6
 #endif
 
 constexpr int kMaxBands = 32;     // one warp lane per radial band
@@ -1160,6 +1163,8 @@ __device__ __forceinline__ void union_window(const QueryArgs& A, const Band& B, 
 constexpr int kBandGroup = HRG_BAND_GROUP;    // bands resolved together (loads in flight)
 constexpr bool kTrimUnion = HRG_TRIM_UNION;   // ... and of the tile's union windows
 constexpr int kUnionSmall = HRG_UNION_SMALL;  // union windows this small are shared by the tile
+constexpr int kDenseMax = HRG_DENSE_MAX;      // ... and up to this size tested as a dense block
+constexpr int kDenseCap = 64;                 // dense candidates per tile (one bit each)
 constexpr int kShareSlack = HRG_SHARE_SLACK;  // (experiment) union shared if it exceeds the
                                               // tile's narrowest window by at most this
 
@@ -1208,9 +1213,11 @@ __device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, i
 }
 
 constexpr int kWalkUnroll = HRG_WALK_UNROLL;  // walk steps whose loads are in flight together
-constexpr int kFirstSeg = 1 << 30;            // flat entry: the query's first segment
-constexpr int kFlatMask = (1 << 21) - 1;      // flat entry: flat index << 5 | lane
-constexpr int kFlatBandShift = 21;            // ... | band << 21 (5 bits)
+// flat entry, second word: flat index of the segment's first candidate
+// (16 bits) | query lane << 16 | band << 21 | the query's first segment << 31
+constexpr int kFirstSeg = INT32_MIN;
+constexpr int kFlatMask = 0xffff;
+constexpr int kFlatLaneShift = 16;
 static_assert(kLightMax * 32 <= (1 << 16), "a tile's flat candidate index must fit 16 bits");
 
 // The walk's pair test with a fixed orientation.  hrgen decides {v, w} with the
@@ -1259,6 +1266,8 @@ struct LightSmem {
   QHot qh[kLightThreads];
   QCold qc[kLightThreads];
   int32_t hits[kLightThreads];
+  int32_t dsh[kLightThreads];                    // dense hits of the warp's queries up to this one
+  int32_t dids[kLightThreads / 32][kDenseCap];   // per warp: ids of the tile's dense candidates
   float dband[kMaxBands];  // e * D of each band's innermost point, rounded up
 };
 
@@ -1326,11 +1335,15 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     const uint32_t* wrowq = A.wtab_q + (wtab_row(A, rvq) - A.wtab);
     // ---- tile-level union windows (lane = band): the 32 queries are
     // angular neighbours, so in bands where their windows are wide relative
-    // to the tile's angular span one resolution serves all of them.  Bands
-    // whose union holds <= kUnionSmall candidates (usually none) are handed
-    // to every query as is; the others are resolved per query.
-    unsigned cheap = 0;
+    // to the tile's angular span the union of the 32 windows is barely larger
+    // than one of them.  Bands whose union is empty are skipped; a union of
+    // at most kDenseMax candidates is tested against all 32 queries as a
+    // dense block (lane = query, the candidates broadcast: no per-query
+    // window, no segment, ~20 instructions per candidate for 32 tests);
+    // the other bands are resolved per query and walked.
+    unsigned cheap = 0, dense = 0, skip = 0;
     int32_t uA = 0, uAe = 0, uB = 0, uBe = 0;
+    int32_t dex = 0, Dn = 0;  // lane = band: first dense-list index of its candidates; their total
     {
       double pmin = active ? phi : 1e300, pmax = active ? phi : -1e300;
       float rmin = rvq, rmax = active ? rvq : 0.0f;
@@ -1341,6 +1354,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         rmin = fminf(rmin, __shfl_xor_sync(FULL, rmin, o));
         rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, o));
       }
+      int32_t un = -1;  // union size; -1: not resolved (the tile spans a wide arc)
       if (pmax >= pmin && pmax - pmin < 0.5 && lane < A.L) {
         const float dlt = __ldg(wtab_row(A, rmin) + lane);
         const double half = 0.5 * (pmax - pmin);
@@ -1354,8 +1368,10 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
           finish_trim(A.keys, r, kA0, kA1, kB0);
         }
         if (r.sB < r.eB && r.sB < r.eA) { r.sA = sb[lane].start; r.eA = sb[lane].end; r.sB = r.eB = 0; }
+        if (r.eA < r.sA) r.eA = r.sA;
+        if (r.eB < r.sB) r.eB = r.sB;
         uA = r.sA; uAe = r.eA; uB = r.sB; uBe = r.eB;
-        const int32_t un = (uAe - uA) + (uBe - uB);
+        un = (uAe - uA) + (uBe - uB);
         // the narrowest window of the tile (its outermost query), in points:
         // if the union exceeds it by little, testing the union costs fewer
         // instructions than resolving 32 windows
@@ -1365,13 +1381,44 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         if (un <= kUnionSmall || (float)un <= w_est + (float)kShareSlack) cheap = 1;
       }
       cheap = __ballot_sync(FULL, cheap != 0);
+      skip = __ballot_sync(FULL, un == 0 || lane >= A.L);
+      bool dn_ok = kDenseMax > 0 && un > 0 && un <= kDenseMax;
+      if (!kSampleIds) {
+        // positions are ids and rows leave sorted: dense hits are written
+        // ahead of a row's walked hits, so dense bands must lie inside every
+        // band that is walked
+        const unsigned walked = __ballot_sync(FULL, lane < A.L && un != 0 && !dn_ok);
+        dn_ok = dn_ok && (walked == 0 || lane < __ffs(walked) - 1);
+      }
+      int32_t dincl = dn_ok ? un : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, dincl, o);
+        if (lane >= o) dincl += y;
+      }
+      // the cap keeps a prefix of the dense bands (indices stay contiguous;
+      // with positions as ids the dropped bands lie outside the kept ones)
+      dn_ok = dn_ok && dincl <= kDenseCap;
+      dense = __ballot_sync(FULL, dn_ok);
+      // non-decreasing over the lanes, for the search below; a band that is
+      // not dense owns no index (it ties with the next dense band, which the
+      // search prefers, or lies past Dn)
+      dex = dincl - (dn_ok ? un : 0);
+      Dn = dense ? __shfl_sync(FULL, dincl, 31 - __clz(dense)) : 0;
     }
-    for (int jg = 0; jg < A.L; jg += kBandGroup) {
+    // bands still to resolve per query (or shared as a small union)
+    for (unsigned todo = ~(skip | dense); todo;) {
+      int jj[kBandGroup];
+#pragma unroll
+      for (int u = 0; u < kBandGroup; ++u) {
+        jj[u] = todo ? __ffs(todo) - 1 : -1;
+        todo &= todo - 1;
+      }
       // union segments of the group's bands, from their lanes
       int32_t gA[kBandGroup], gAe[kBandGroup], gB[kBandGroup], gBe[kBandGroup];
 #pragma unroll
       for (int u = 0; u < kBandGroup; ++u) {
-        const int j = min(jg + u, 31);
+        const int j = max(jj[u], 0);
         gA[u] = __shfl_sync(FULL, uA, j); gAe[u] = __shfl_sync(FULL, uAe, j);
         gB[u] = __shfl_sync(FULL, uB, j); gBe[u] = __shfl_sync(FULL, uBe, j);
       }
@@ -1383,9 +1430,9 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         RawWin w[kBandGroup];
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
-          const int j = jg + u;
+          const int j = jj[u];
           w[u] = RawWin{0, 0, 0, 0, 0, kQMask + 1, 0};
-          if (j >= A.L || ((cheap >> j) & 1u)) continue;
+          if (j < 0 || ((cheap >> j) & 1u)) continue;
           const uint32_t dq = __ldg(wrowq + j);
           const int32_t bs = sb[j].start, be = sb[j].end;
           if (dq == kWinEmpty || be <= bs) continue;
@@ -1400,8 +1447,8 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         }
 #pragma unroll
         for (int u = 0; u < kBandGroup; ++u) {
-          const int j = jg + u;
-          if (j >= A.L) continue;
+          const int j = jj[u];
+          if (j < 0) continue;
           RawWin& r = w[u];
           if ((cheap >> j) & 1u) {
             r.sA = gA[u]; r.eA = gAe[u]; r.sB = gB[u]; r.eB = gBe[u];
@@ -1423,8 +1470,9 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         }
       }
     }
-    cand_local += (unsigned long long)c;
-    const bool heavy = active && (c > kLightMax || ovf);
+    // every query of the tile also tests the Dn dense candidates
+    cand_local += active ? (unsigned long long)(c + Dn) : 0ull;
+    const bool heavy = active && (c + Dn > kLightMax || ovf);
     const bool light = active && !heavy;
     const int32_t want = light ? c : 0, nsl = light ? nseg : 0;
     int32_t incl = want, sincl = nsl;  // inclusive scans: candidates, segments
@@ -1435,38 +1483,91 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     }
     const int32_t T = __shfl_sync(FULL, incl, 31), S = __shfl_sync(FULL, sincl, 31);
     const int32_t excl = incl - want;
+    int2* fl = sm.flat[tid >> 5];
+    QFull f;
+    float invd = 0.0f;
+    if (light) {
+      f = load_query<kSampleIds>(A, v);
+      invd = A.q.invd[v];
+      QHot h;
+      h.cx = f.cx; h.cy = f.cy; h.rsq = f.rsq; h.invd = invd; h.idv = f.idv;
+      sm.qh[tid] = h;
+      QCold k;
+      k.px = f.px; k.py = f.py;
+      sm.qc[tid] = k;
+    }
+    // ---- dense block: lane k of each half holds dense candidate k (its band
+    // from a search over the bands' first indices), every candidate is
+    // broadcast and tested by all lanes against their own query.  Bit k of
+    // dm: candidate k is a neighbour of this lane's query.
+    unsigned long long dm = 0;
+    for (int h0 = 0; h0 < Dn; h0 += 32) {
+      const int k = h0 + lane;
+      int l = 0;  // owner band: the last lane with dex <= k
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1)
+        if (__shfl_sync(FULL, dex, l + st) <= k) l += st;
+      const int32_t t = k - __shfl_sync(FULL, dex, l);
+      const int32_t la = __shfl_sync(FULL, uAe - uA, l);
+      const int32_t pa = __shfl_sync(FULL, uA, l), pb = __shfl_sync(FULL, uB, l);
+      const int32_t pos = k < Dn ? (t < la ? pa + t : pb + (t - la)) : 0;
+      const double2 cp = __ldg(A.rec.pt + pos);
+      const int32_t cid = kSampleIds ? __ldg(A.rec.ids + pos) : pos;
+      const float ced = sm.dband[l];
+      if (k < Dn) sm.dids[tid >> 5][k] = cid;
+      const int nk = min(32, Dn - h0);
+      for (int kk = 0; kk < nk; ++kk) {
+        const double px = __shfl_sync(FULL, cp.x, kk), py = __shfl_sync(FULL, cp.y, kk);
+        const int32_t idw = __shfl_sync(FULL, cid, kk);
+        const float ed = __shfl_sync(FULL, ced, kk);
+        const int32_t pw = __shfl_sync(FULL, pos, kk);
+        if (light) {
+          const double dx = __dsub_rn(px, f.cx), dy = __dsub_rn(py, f.cy);
+          const double s2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+          bool hit = s2 < f.rsq;  // quadtree.py:611-613 with v's circle
+          if (idw < f.idv &&
+              fabsf(__double2float_rn(__dsub_rn(s2, f.rsq))) <= fmaf(ed, invd, kPredErrF)) {
+            double2 oc;
+            double orsq;
+            load_other<kSampleIds>(A.rec, pw, oc, orsq);
+            hit = ref_pred(f.px, f.py, oc.x, oc.y, orsq);  // w's circle decides
+          }
+          if (hit && idw != f.idv) dm |= 1ull << (h0 + kk);
+        }
+      }
+    }
+    const int32_t dh = __popcll(dm);
+    int32_t dhi = dh;  // inclusive scan of the dense hits over the tile's queries
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(FULL, dhi, o);
+      if (lane >= o) dhi += y;
+    }
+    sm.dsh[tid] = dhi;
+    // staging for the tile's light rows: walked candidates + dense hits
+    const int32_t Talloc = T + __shfl_sync(FULL, dhi, 31);
     unsigned long long base = 0;
-    if (lane == 31 && T > 0) base = atomicAdd(A.bump, (unsigned long long)T);
+    if (lane == 31 && Talloc > 0) base = atomicAdd(A.bump, (unsigned long long)Talloc);
     base = __shfl_sync(FULL, base, 31);
     sm.hits[tid] = 0;
     if (heavy) {
-      unsigned long long hoff = atomicAdd(A.bump, (unsigned long long)c);
+      unsigned long long hoff = atomicAdd(A.bump, (unsigned long long)(c + Dn));
       unsigned e = atomicAdd(A.heavy_n, 1u);
       A.heavy_v[e] = v;
-      A.heavy_c[e] = c;
+      A.heavy_c[e] = c + Dn;
       A.heavy_of[v] = (int32_t)e;
       A.stage_off[v] = (int64_t)hoff;
-      A.slots[v] = c;
+      A.slots[v] = c + Dn;
     } else if (active) {
       A.heavy_of[v] = -1;
     }
-    const bool fits = (int64_t)base + T <= A.stage_cap;
+    const bool fits = (int64_t)base + Talloc <= A.stage_cap;
     if (!fits && lane == 0) atomicOr(A.overflow, 1);
     // ---- flatten: lane l's segments sit at fl[l * kSegStride + k] as (first
     // record, offset in the query).  Pack them, in query order, to fl[0, S)
     // as (first record, kFirstSeg | flat index of the first candidate << 5 |
     // lane).  Rounds run over destinations; every entry moves down (dest <=
     // source), so a round's writes never hit a source still to be read.
-    int2* fl = sm.flat[tid >> 5];
-    if (light) {
-      const QFull f = load_query<kSampleIds>(A, v);
-      QHot h;
-      h.cx = f.cx; h.cy = f.cy; h.rsq = f.rsq; h.invd = A.q.invd[v]; h.idv = f.idv;
-      sm.qh[tid] = h;
-      QCold k;
-      k.px = f.px; k.py = f.py;
-      sm.qc[tid] = k;
-    }
     {
       const int32_t sb = sincl - nsl;
       for (int e0 = 0; e0 < S; e0 += 32) {
@@ -1481,17 +1582,20 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         if (e < S) g = fl[l * kSegStride + k];
         __syncwarp();
         if (e < S)
-          fl[e] = make_int2(g.x, (k == 0 ? kFirstSeg : 0) | ((g.y >> 16) << kFlatBandShift) |
-                                     ((own_ex + (g.y & 0xffff)) << 5) | l);
+          fl[e] = make_int2(g.x, (k == 0 ? kFirstSeg : 0) | ((g.y >> 16) << (kFlatLaneShift + 5)) |
+                                     (l << kFlatLaneShift) | (own_ex + (g.y & 0xffff)));
         __syncwarp();
       }
     }
+    __syncwarp();
     // ---- walk: lane l takes flat candidate i0 + l, so a warp reads 32
     // consecutive records of one or a few segments per step.  The segment of
     // each lane comes from a bit mask of the segment starts inside the step.
     // Only hits are written, compacted, so a query's hits are one contiguous
     // run; the running hit prefix at a query's first and past its last
-    // candidate bound that run.
+    // candidate bound that run.  A query's dense hits go in front of its
+    // walked ones: a walked hit moves up by the dense hits of the queries up
+    // to and including its own.
     if (fits) {
       int32_t* out = A.stage + base;
       int s0 = 0;          // segment holding flat index i0
@@ -1504,16 +1608,15 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         for (int u = 0; u < kWalkUnroll; ++u) {
           const int32_t ib = i0 + 32 * u;
           const int sl = s0 + 1 + lane;
-          const int32_t st = sl < S ? ((fl[sl].y & kFlatMask) >> 5) : INT32_MAX;
+          const int32_t st = sl < S ? (fl[sl].y & kFlatMask) : INT32_MAX;
           const unsigned rel = (unsigned)(st - ib);
           const unsigned mask = __reduce_or_sync(FULL, rel < 32u ? 1u << rel : 0u);
           const int my = s0 + __popc(mask & ((2u << lane) - 1u));
           s0 += __popc(mask);
           const int2 e = fl[my];
-          const int32_t off = ib + lane - ((e.y & kFlatMask) >> 5);
-          // query lane | band << 5 | first candidate of its query << 10
-          qv[u] = (e.y & 31) | (((e.y >> kFlatBandShift) & 31) << 5);
-          qs[u] = off == 0 && (e.y & kFirstSeg);
+          const int32_t off = ib + lane - (e.y & kFlatMask);
+          qv[u] = (e.y >> kFlatLaneShift) & 1023;  // query lane | band << 5
+          qs[u] = off == 0 && e.y < 0;              // first candidate of its query
           wv[u] = e.x + off;
         }
         double2 pt[kWalkUnroll];
@@ -1537,41 +1640,49 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
             unc[u] = idw[u] < f.idv && g <= fmaf(sm.dband[qv[u] >> 5], f.invd, kPredErrF);
           }
         }
-        // margin cases (rare): w's circle decides.  Their loads are issued
-        // together and waited for once per group of steps.
-        double2 oc[kWalkUnroll];
-        double orsq[kWalkUnroll];
+        // margin cases (rare: one group of steps in ~4 holds any): w's circle
+        // decides.  Their loads are issued together and waited for once.
+        bool any_unc = false;
 #pragma unroll
-        for (int u = 0; u < kWalkUnroll; ++u)
-          if (unc[u]) load_other<kSampleIds>(A.rec, wv[u], oc[u], orsq[u]);
+        for (int u = 0; u < kWalkUnroll; ++u) any_unc = any_unc || unc[u];
+        if (__any_sync(FULL, any_unc)) {
+          double2 oc[kWalkUnroll];
+          double orsq[kWalkUnroll];
 #pragma unroll
-        for (int u = 0; u < kWalkUnroll; ++u)
-          if (unc[u]) {
-            const QCold k = sm.qc[wb + (qv[u] & 31)];
-            hit[u] = ref_pred(k.px, k.py, oc[u].x, oc[u].y, orsq[u]);
-          }
+          for (int u = 0; u < kWalkUnroll; ++u)
+            if (unc[u]) load_other<kSampleIds>(A.rec, wv[u], oc[u], orsq[u]);
+#pragma unroll
+          for (int u = 0; u < kWalkUnroll; ++u)
+            if (unc[u]) {
+              const QCold k = sm.qc[wb + (qv[u] & 31)];
+              hit[u] = ref_pred(k.px, k.py, oc[u].x, oc[u].y, orsq[u]);
+            }
+        }
 #pragma unroll
         for (int u = 0; u < kWalkUnroll; ++u) {
           const int32_t i = i0 + 32 * u + lane;
           // hits only, compacted: the tile's rows end up back to back
           const unsigned hm = __ballot_sync(FULL, hit[u]);
           const int32_t at = pre + __popc(hm & ((1u << lane) - 1u));
-          if (hit[u]) out[at] = idw[u];
+          if (hit[u]) out[at + sm.dsh[wb + (qv[u] & 31)]] = idw[u];
           if (qs[u] && i < T) sm.hits[wb + (qv[u] & 31)] = at;
           pre += __popc(hm);
         }
       }
-      // hits of query q = prefix at the next non-empty query (or the end)
-      // minus the prefix at q
+      // walked hits of query q = prefix at the next non-empty query (or the
+      // end) minus the prefix at q; the row is its dense hits, then those
       __syncwarp();
       const unsigned ne = __ballot_sync(FULL, want > 0) & ~((2u << lane) - 1u);
-      const int32_t mine = sm.hits[tid];
       const int32_t end = ne ? sm.hits[wb + __ffs(ne) - 1] : pre;
+      const int32_t mine = want > 0 ? sm.hits[tid] : end;
       __syncwarp();
-      sm.hits[tid] = want > 0 ? end - mine : 0;
+      const int32_t row0 = mine + dhi - dh;  // the row's first slot in the tile's range
+      sm.hits[tid] = end - mine + dh;
+      for (unsigned long long m = dm; m; m &= m - 1)
+        out[row0 + __popcll(dm & ((m & -m) - 1))] = sm.dids[tid >> 5][__ffsll((long long)m) - 1];
       if (light) {  // the row's hits: stage[stage_off, stage_off + slots)
-        A.stage_off[v] = (int64_t)base + (want > 0 ? mine : 0);
-        A.slots[v] = want > 0 ? end - mine : 0;
+        A.stage_off[v] = (int64_t)base + row0;
+        A.slots[v] = end - mine + dh;
       }
     }
     __syncwarp();
