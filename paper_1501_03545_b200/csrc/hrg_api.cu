@@ -81,7 +81,7 @@ struct hrg_context {
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits, chunk_entry,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
-      sub_off, sub_len, sub_cur, chunk_row, tk0, tv0, wtab, job_dst, job_len, mid_off, mid_len;
+      sub_off, sub_len, sub_cur, chunk_row, tv0, wtab, job_dst, job_len, mid_off, mid_len;
   int64_t stage_cap = 0;
   // index
   Buf bands, dir, dir_total, bad, dir_gaps, band_pmin;
@@ -344,15 +344,15 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
       A.bands, L, rows, M->cosh_r_minus_1, std::ldexp(1.0, -45), c->wtab.as<float>(),
       reinterpret_cast<uint32_t*>(c->wtab.as<float>() + (size_t)rows * L));
 
-  // query tiles: 32 consecutive positions of one band, band after band
-  // (interleaving the bands' tiles by angle cuts DRAM reads by 40% but
-  // measured slower: the tiles in flight then mix wide and narrow windows)
+  // query tiles: 32 consecutive positions of one band; inner bands in band
+  // order, the outermost kTileMixBands interleaved by angle (k_tile_table)
   {
     const int64_t ntmax = np / 32 + L + 1;
-    CUDA_TRY(c->tk0.ensure(8 * (size_t)ntmax));
     CUDA_TRY(c->tv0.ensure(8 * (size_t)ntmax));
-    ++c->launches, k_tile_keys<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
-        A.bands, L, A.keys, ntmax, c->tk0.as<uint64_t>(), c->tv0.as<uint64_t>());
+    int first_mixed = std::max(0, L - kTileMixBands);
+    if (const char* e = getenv("HRG_TILE_MIX")) first_mixed = std::max(0, L - atoi(e));
+    ++c->launches, k_tile_table<<<(unsigned)std::min<int64_t>(blocks_for(ntmax), 4 * c->sm_count), 256, 0, st>>>(
+        A.bands, L, ntmax, c->tv0.as<uint64_t>(), first_mixed);
     A.tiles = c->tv0.as<uint64_t>();
     A.ntiles = ntmax;
   }
@@ -919,7 +919,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_entry, &c->chunk_off,
                  &c->slots,
                  &c->large_off, &c->large_len, &c->giant_off, &c->giant_len, &c->giant_meta, &c->sub_off, &c->sub_len, &c->sub_cur,
-                 &c->chunk_row, &c->tk0, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
+                 &c->chunk_row, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps, &c->band_pmin,
                  &c->deg, &c->rowptr, &c->idx, &c->cand, &c->rowidx, &c->row_ids, &c->rowptr_c, &c->nq_buf, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
                  &c->widen})

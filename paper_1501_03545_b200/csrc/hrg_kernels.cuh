@@ -12,7 +12,7 @@
 //                    correctly rounded sin/cos, hrgen's circle transform
 //                    (geometry.py:141-157); per-band innermost radius.
 //   k_band_setup / k_dir_fill / k_dir_gaps / k_dir_tail / k_window_table /
-//   k_tile_keys      per band: position and sector ranges, an angular
+//   k_tile_table     per band: position and sector ranges, an angular
 //                    directory (bucket -> first position); per query-radius row
 //                    and band: the angular half-width of a conservative window;
 //                    query tiles (32 consecutive positions of one band).
@@ -39,7 +39,7 @@ namespace hrg {
 
 // tuning knobs (-D overrides for experiments)
 #ifndef HRG_WALK_UNROLL
-#define HRG_WALK_UNROLL 3
+#define HRG_WALK_UNROLL 2
 #endif
 #ifndef HRG_BAND_GROUP
 #define HRG_BAND_GROUP 1
@@ -72,7 +72,7 @@ namespace hrg {
 #define HRG_COMPACT_MINB 5
 #endif
 #ifndef HRG_SEGCAP
-#define HRG_SEGCAP 20
+#define HRG_SEGCAP 16
 #endif
 #ifndef HRG_LIGHT_MAX
 #define HRG_LIGHT_MAX 2048
@@ -96,7 +96,7 @@ namespace hrg {
 #define HRG_HEAVY_BATCH 4
 #endif
 #ifndef HRG_LIGHT_MINBLOCKS
-#define HRG_LIGHT_MINBLOCKS 6
+#define HRG_LIGHT_MINBLOCKS 7
 #endif
 
 constexpr int kMaxBands = 32;     // one warp lane per radial band
@@ -647,12 +647,22 @@ __global__ void k_rowidx(const Band* __restrict__ bands, int L, const int32_t* _
   }
 }
 
-// Tile table: every band's query range cut into tiles of 32 positions (the
-// key is the angular key of the tile's first point, for an angular
-// interleave of the bands' tiles; unused -- see hrg_api.cu).
-__global__ void k_tile_keys(const Band* __restrict__ bands, int L, const uint64_t* __restrict__ keys,
-                            int64_t ntmax, uint64_t* __restrict__ tkey,
-                            uint64_t* __restrict__ tval) {
+// Tile table: every band's query range cut into tiles of 32 positions.  The
+// light pass takes tiles in table order.  Bands below first_mixed come band
+// after band (the inner bands' tiles are the expensive ones and start first);
+// the tiles of the outer bands, which hold nearly all points, are interleaved
+// by their relative position in the band -- their angle, up to sampling noise --
+// so the tiles in flight share one angular sector of every band and the L2
+// serves the sweep (one pass over the records instead of one per query band).
+// The interleave is a rank, not a sort: tile t of nt_j precedes tile t' of
+// nt_j' iff (2t + 1) nt_j' < (2t' + 1) nt_j, ties by band -- a total order on
+// exact integers, so the ranks are a permutation.
+#ifndef HRG_TILE_MIX
+#define HRG_TILE_MIX 5
+#endif
+constexpr int kTileMixBands = HRG_TILE_MIX;  // outermost bands whose tiles interleave
+__global__ void k_tile_table(const Band* __restrict__ bands, int L, int64_t ntmax,
+                             uint64_t* __restrict__ tval, int first_mixed) {
   __shared__ int64_t pre[kMaxBands + 1];
   if (threadIdx.x == 0) {
     int64_t a = 0;
@@ -666,16 +676,29 @@ __global__ void k_tile_keys(const Band* __restrict__ bands, int L, const uint64_
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < ntmax;
        k += (int64_t)gridDim.x * blockDim.x) {
     if (k >= pre[L]) {
-      tkey[k] = (1ull << 54) - 1;  // sorts last
       tval[k] = ~0ull;
       continue;
     }
     int j = 0;
     while (j + 1 < L && pre[j + 1] <= k) ++j;
-    const int64_t s = bands[j].qstart + (k - pre[j]) * 32;
+    const int64_t t = k - pre[j];
+    const int64_t s = bands[j].qstart + t * 32;
     const int64_t e = min(s + 32, (int64_t)bands[j].qend);
-    tkey[k] = __ldg(keys + s) & kQMask;
-    tval[k] = (uint64_t)s | ((uint64_t)e << 32);
+    int64_t rank = k;
+    if (j >= first_mixed) {
+      const int64_t nt = pre[j + 1] - pre[j];
+      rank = pre[first_mixed];
+      for (int jj = first_mixed; jj < L; ++jj) {
+        const int64_t ntj = pre[jj + 1] - pre[jj];
+        if (jj == j) { rank += t; continue; }
+        // tiles t' of band jj ahead of (j, t): (2t' + 1) nt < (2t + 1) ntj,
+        // or <= when jj < j
+        const int64_t B = (2 * t + 1) * ntj;
+        const int64_t q = jj < j ? B / nt : (B - 1) / nt;  // 2t' + 1 <= q
+        rank += min(ntj, (q + 1) / 2);
+      }
+    }
+    tval[rank] = (uint64_t)s | ((uint64_t)e << 32);
   }
 }
 
@@ -1255,7 +1278,7 @@ constexpr float kPredErrF = 0x1.000008p-45f;  // e, rounded up
 constexpr int kSegCapWide = HRG_WIDE_CAP;   // static shared memory stays under 48 KB
 constexpr int kWideMinBlocks = HRG_WIDE_MINB;
 #ifndef HRG_SEGCAP_SHARD
-#define HRG_SEGCAP_SHARD 24
+#define HRG_SEGCAP_SHARD 16
 #endif
 constexpr int kSegCapShard = HRG_SEGCAP_SHARD;  // sharded runs (few tiles per warp)
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
@@ -1600,10 +1623,13 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
       int32_t* out = A.stage + base;
       int s0 = 0;          // segment holding flat index i0
       int32_t pre = 0;     // hits before i0
-      for (int32_t i0 = 0; i0 < T; i0 += 32 * kWalkUnroll) {
-        int32_t wv[kWalkUnroll];
-        int qv[kWalkUnroll];
-        bool qs[kWalkUnroll];
+      // the segment lookup of a group of steps: each lane's candidate (wv),
+      // its query lane | band << 5 (qv), first candidate of its query (qs)
+      int32_t wv[kWalkUnroll], nwv[kWalkUnroll];
+      int qv[kWalkUnroll], nqv[kWalkUnroll];
+      bool qs[kWalkUnroll], nqs[kWalkUnroll];
+      auto lookup = [&](int32_t i0, int32_t (&w)[kWalkUnroll], int (&q)[kWalkUnroll],
+                        bool (&first)[kWalkUnroll]) {
 #pragma unroll
         for (int u = 0; u < kWalkUnroll; ++u) {
           const int32_t ib = i0 + 32 * u;
@@ -1611,14 +1637,19 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
           const int32_t st = sl < S ? (fl[sl].y & kFlatMask) : INT32_MAX;
           const unsigned rel = (unsigned)(st - ib);
           const unsigned mask = __reduce_or_sync(FULL, rel < 32u ? 1u << rel : 0u);
-          const int my = s0 + __popc(mask & ((2u << lane) - 1u));
+          const int my = min(s0 + __popc(mask & ((2u << lane) - 1u)), max(S - 1, 0));
           s0 += __popc(mask);
           const int2 e = fl[my];
           const int32_t off = ib + lane - (e.y & kFlatMask);
-          qv[u] = (e.y >> kFlatLaneShift) & 1023;  // query lane | band << 5
-          qs[u] = off == 0 && e.y < 0;              // first candidate of its query
-          wv[u] = e.x + off;
+          q[u] = (e.y >> kFlatLaneShift) & 1023;
+          first[u] = off == 0 && e.y < 0;
+          w[u] = e.x + off;
         }
+      };
+      lookup(0, nwv, nqv, nqs);
+      for (int32_t i0 = 0; i0 < T; i0 += 32 * kWalkUnroll) {
+#pragma unroll
+        for (int u = 0; u < kWalkUnroll; ++u) { wv[u] = nwv[u]; qv[u] = nqv[u]; qs[u] = nqs[u]; }
         double2 pt[kWalkUnroll];
         int32_t idw[kWalkUnroll];
 #pragma unroll
@@ -1627,6 +1658,8 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
             pt[u] = __ldg(A.rec.pt + wv[u]);
             idw[u] = kSampleIds ? __ldg(A.rec.ids + wv[u]) : wv[u];
           }
+        // the next group's lookup (shared memory) runs under these loads
+        if (i0 + 32 * kWalkUnroll < T) lookup(i0 + 32 * kWalkUnroll, nwv, nqv, nqs);
         bool hit[kWalkUnroll], unc[kWalkUnroll];
 #pragma unroll
         for (int u = 0; u < kWalkUnroll; ++u) {
