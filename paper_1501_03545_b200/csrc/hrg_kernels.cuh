@@ -90,7 +90,7 @@ namespace hrg {
 #define HRG_SORT_GRID 12
 #endif
 #ifndef HRG_HEAVY_MINB
-#define HRG_HEAVY_MINB 2
+#define HRG_HEAVY_MINB 3
 #endif
 #ifndef HRG_HEAVY_BATCH
 #define HRG_HEAVY_BATCH 4
@@ -1823,10 +1823,14 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
     const int32_t v = A.heavy_v[e];
     const int64_t local = c - A.chunk_start[e];
     QFull f = load_query<kSampleIds>(A, v);
+    const float invd = A.q.invd[v];
     int32_t sA = 0, eA = 0, sB = 0, eB = 0;
+    float ed = 0.0f;  // lane = band: e * D of its innermost point (the walk's margin)
     if (lane < A.L) {
       const float* wrow = wtab_row(A, A.q.rf[v]);
       union_window(A, sb[lane], A.q.phi[v], __ldg(wrow + lane), sA, eA, sB, eB);
+      const double D = A.a * ((1.0 - sb[lane].pmin) * (1.0 + sb[lane].pmin)) + 2.0;
+      ed = __double2float_ru(0x1p-45 * D) * (1.0f + 0x1p-18f);
     }
     const int32_t lenA = eA - sA, cnt = lenA + (eB - sB);
     int32_t incl = cnt;
@@ -1846,6 +1850,7 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
     for (int32_t base = beg; base < end; base += 32 * HB) {
       int32_t wv[HB];
       bool ok[HB];
+      float edw[HB];
 #pragma unroll
       for (int u = 0; u < HB; ++u) {
         int32_t i = base + 32 * u + lane;
@@ -1859,18 +1864,38 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
         int32_t la = __shfl_sync(FULL, lenA, o);
         int32_t sa = __shfl_sync(FULL, sA, o);
         int32_t sbb = __shfl_sync(FULL, sB, o);
+        edw[u] = __shfl_sync(FULL, ed, o);
         wv[u] = tt < la ? sa + tt : sbb + (tt - la);
         ok[u] = i < end;
       }
-      Cand r[HB];
+      // the walk's test (see QHot): v's circle against w's point, the other
+      // orientation only inside the rounding margin
+      double2 pt[HB];
+      int32_t idw[HB];
 #pragma unroll
       for (int u = 0; u < HB; ++u)
-        if (ok[u]) r[u] = load_cand<kSampleIds>(A, f, wv[u]);
+        if (ok[u]) {
+          pt[u] = __ldg(A.rec.pt + wv[u]);
+          idw[u] = kSampleIds ? __ldg(A.rec.ids + wv[u]) : wv[u];
+        }
 #pragma unroll
       for (int u = 0; u < HB; ++u) {
-        bool hit = ok[u] && pair_test(f, r[u], wv[u]);
+        bool hit = false;
+        if (ok[u]) {
+          const double dx = __dsub_rn(pt[u].x, f.cx), dy = __dsub_rn(pt[u].y, f.cy);
+          const double s2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+          hit = s2 < f.rsq;
+          if (idw[u] < f.idv &&
+              fabsf(__double2float_rn(__dsub_rn(s2, f.rsq))) <= fmaf(edw[u], invd, kPredErrF)) {
+            double2 oc;
+            double orsq;
+            load_other<kSampleIds>(A.rec, wv[u], oc, orsq);
+            hit = ref_pred(f.px, f.py, oc.x, oc.y, orsq);
+          }
+          hit = hit && idw[u] != f.idv;
+        }
         unsigned bal = __ballot_sync(FULL, hit);
-        if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = r[u].id;
+        if (hit && fits) out[hits + __popc(bal & ((1u << lane) - 1u))] = idw[u];
         hits += __popc(bal);
       }
     }
