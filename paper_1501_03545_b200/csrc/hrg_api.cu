@@ -288,7 +288,7 @@ hrg_status scan_i32_to_i64(hrg_context* c, const int32_t* in, int64_t* out, int6
 // Light query pass, heavy (hub) pass, scans, compaction (+ row sort when ids
 // are not positions).
 hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool sample_ids,
-                      bool compact, hrg_stats* stats) {
+                      bool compact, int shard_count, hrg_stats* stats) {
   const int64_t n = M->n;   // vertex ids (rows)
   const int64_t np = c->np; // indexed positions
   cudaStream_t st = c->stream;
@@ -298,6 +298,13 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
                 c->vals_out.as<int32_t>()};
   A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_invd.as<float>()};
   A.a = M->cosh_r_minus_1;
+  // one warp walks a whole tile, so a tile of 32 queries at the limit bounds
+  // the light pass from below (~0.35 ms at 2048): sharded runs, whose light
+  // pass is that short, defer earlier (the heavy pass spreads a query's
+  // chunks over the machine)
+  A.light_max = kLightMax;
+  if (shard_count > 1) A.light_max = std::min(kLightMax, std::max(512, 2 * kLightMax / shard_count));
+  if (const char* e = getenv("HRG_LIGHT_MAX")) A.light_max = std::min(kLightMax, std::max(32, atoi(e)));
   A.bands = c->bands.as<Band>();
   A.dir = c->dir.as<int32_t>();
   A.keys = c->keys_out.as<uint64_t>();
@@ -821,7 +828,8 @@ hrg_status run_pipeline(hrg_context* c, const hrg_model* M, const hrg_shard* sha
   }
   s = build_index(c, M, S, L, shard, C, sample_ids);
   if (s != HRG_OK) return s;
-  s = emit_edges(c, M, L, C, sample_ids, shard && shard->count > 1 && sample_ids, stats);
+  s = emit_edges(c, M, L, C, sample_ids, shard && shard->count > 1 && sample_ids,
+                 shard ? shard->count : 1, stats);
   if (s != HRG_OK) return s;
   CUDA_TRY(cudaStreamSynchronize(st));
   c->n = n;

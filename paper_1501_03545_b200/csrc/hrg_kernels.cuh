@@ -579,6 +579,7 @@ struct QueryArgs {
   int L;
   double C;                  // 2^53 / (2 pi)
   double a;                  // 2 sinh^2(R/2) = cosh R - 1 (geometry.py:149)
+  int32_t light_max;         // queries with more candidates are deferred (<= kLightMax)
   // staging: every light query owns one slot per candidate (hit id or -1);
   // a heavy query's slice holds its chunks' compacted hits at chunk * kChunk
   int32_t* stage;
@@ -1495,7 +1496,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     }
     // every query of the tile also tests the Dn dense candidates
     cand_local += active ? (unsigned long long)(c + Dn) : 0ull;
-    const bool heavy = active && (c + Dn > kLightMax || ovf);
+    const bool heavy = active && (c + Dn > A.light_max || ovf);
     const bool light = active && !heavy;
     const int32_t want = light ? c : 0, nsl = light ? nseg : 0;
     int32_t incl = want, sincl = nsl;  // inclusive scans: candidates, segments

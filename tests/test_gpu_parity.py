@@ -223,13 +223,32 @@ def test_generate_matches_oracle(oracle, kw):
 @pytest.mark.parametrize("kw", [GEN_CASES[1], GEN_CASES[2], GEN_CASES[5]],
                          ids=["k32-g2.5", "k4-g2.2", "R35.5"])
 def test_light_query_variants_match_oracle(oracle, kw, wide, monkeypatch):
-    """Both light-query variants (28 and 36 segment slots; the model picks
+    """Both light-query variants (16 and 36 segment slots; the model picks
     one, HRG_LIGHT_WIDE forces it) give the oracle's edge set exactly."""
     monkeypatch.setenv("HRG_LIGHT_WIDE", wide)
     p = GeneratorParams(**kw)
     model = p.resolve()
     g = P.generate(p)
     co = P.sample_points(model.n, model.alpha, model.R, p.seed)
+    a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
+    e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
+                                    P.to_poincare_radius(model.R), 512, oracle.TRIG_LIBM)
+    assert g.m == m and np.array_equal(g.edge_array(), e)
+
+
+@pytest.mark.parametrize("mix", ["0", "3", "32"])
+@pytest.mark.parametrize("order", ["sample", "angular"])
+def test_tile_order_and_dense_block_match_oracle(oracle, mix, order, monkeypatch):
+    """The light pass's tile table (outermost HRG_TILE_MIX bands interleaved by
+    an exact rank: every tile must appear exactly once) and its dense block
+    (small tile-union windows tested by all 32 queries; with angular ids only
+    bands inside every walked band, so rows leave sorted) give the oracle's
+    edge set on the GPU's own coordinates, in both vertex orders."""
+    monkeypatch.setenv("HRG_TILE_MIX", mix)
+    p = GeneratorParams(n=300_000, avg_degree=24.0, gamma=2.6, seed=11, vertex_order=order)
+    model = p.resolve()
+    g, co = P.generate_with_coordinates(p)
+    check_csr(g)
     a = P.model_constants(model.R, model.alpha)["cosh_r_minus_1"]
     e, m, _ = oracle.edges_quadtree(co.phi, co.r_poincare, a, model.alpha,
                                     P.to_poincare_radius(model.R), 512, oracle.TRIG_LIBM)
