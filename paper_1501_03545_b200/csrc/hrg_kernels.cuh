@@ -7,20 +7,25 @@
 //                    Sharded runs: k_shard_keys / k_shard_select /
 //                    k_shard_points keep only the points the sector can reach.
 //   cub radix sort   keys -> permutation into (band, angle) order.
-//   k_gather         48-byte fp64 candidate records in sorted order: p_x, p_y
-//                    (the point), c_x, c_y, rad^2 (its query circle), id;
-//                    correctly rounded sin/cos, hrgen's circle transform
-//                    (geometry.py:141-157); per-band innermost radius.
+//   k_gather         fp64 records in sorted order: the 16-byte point (p_x, p_y)
+//                    every pair test reads, and the 48-byte full record (point,
+//                    query circle c_x, c_y, rad^2, id) of the query side and the
+//                    rare other-orientation test; glibc's sin/cos bit for bit,
+//                    hrgen's circle transform (geometry.py:141-157); per-band
+//                    innermost radius; 1/D per point (the test's margin).
 //   k_band_setup / k_dir_fill / k_dir_gaps / k_dir_tail / k_window_table /
 //   k_tile_table     per band: position and sector ranges, an angular
 //                    directory (bucket -> first position); per query-radius row
 //                    and band: the angular half-width of a conservative window;
-//                    query tiles (32 consecutive positions of one band).
-//   k_light          a warp per tile: per-band windows (shared by the tile where
-//                    the union is tiny), segments flattened, a lane-strided walk
-//                    over the candidates with the reference predicate, hits
-//                    compacted into staging; queries with too many candidates or
-//                    segments are deferred.
+//                    query tiles (32 consecutive positions of one band; the
+//                    outer bands' tiles interleaved by angle).
+//   k_light          a warp per tile: per-band union windows; small unions
+//                    tested as a dense block (lane = query), the other bands
+//                    resolved per query (integer windows), segments flattened,
+//                    a lane-strided walk over the candidates; the reference
+//                    predicate in one orientation (the other inside the
+//                    rounding margin), hits compacted into staging; queries
+//                    with too many candidates or segments are deferred.
 //   k_heavy          a warp per 2048-candidate chunk of a deferred query (hubs).
 //   cub scan         degrees -> CSR row pointers (+ per-chunk offsets of hubs).
 //   k_compact_light / k_compact_heavy   staging -> CSR rows; rows of <= 64 ids
