@@ -114,7 +114,7 @@ struct hrg_context {
   int64_t launches = 0;  // this library's kernel launches (CUB's not included)
   int trig = kTrigLibm;  // sin/cos of the Poincare coordinates (hrg_context_set_trig)
   int grid_block_count = 0, grid_block_write = 0;
-  int grid_light = 0, grid_light_wide = 0, grid_light_shard = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
+  int grid_light = 0, grid_light_wide = 0, grid_light_steep = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
 namespace {
@@ -373,8 +373,8 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
 #endif
     c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, kWideMinBlocks>, kLightThreads);
-    c->grid_light_shard =
-        occupancy_grid(c, k_light<true, kSegCapShard, HRG_LIGHT_MINBLOCKS>, kLightThreads);
+    c->grid_light_steep =
+        occupancy_grid(c, k_light<true, kSegCapSteep, kSteepMinBlocks>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact_heavy = occupancy_grid(c, k_compact_heavy);
 #ifdef HRG_COMPACT_CARVEOUT
@@ -414,14 +414,15 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     wide = populated >= kWideBands;
     if (const char* e = getenv("HRG_LIGHT_WIDE")) wide = atoi(e) != 0;
   }
-  // a sharded run has ~8x fewer tiles per warp, and there the 4 extra slots
-  // of kSegCap cost more in the light pass (measured: 0.49 -> 0.69 ms per
-  // rank at config 2, N = 8) than the deferrals they save
-  const bool shard_slots = !wide && np < n;
+  // steep degree distributions: fewer slots, one more resident block
+  // (measured at k = 4 / 16 / 64, gamma = 3: light pass -4..-6%; at
+  // gamma = 2.5 the extra deferrals cost more than the light pass gains)
+  bool steep = !wide && M->alpha >= 0.95;
+  if (const char* e = getenv("HRG_LIGHT_STEEP")) steep = !wide && atoi(e) != 0;
   unsigned gq = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kLightThreads),
                            wide ? c->grid_light_wide
-                                : (shard_slots ? c->grid_light_shard : c->grid_light)));
+                                : (steep ? c->grid_light_steep : c->grid_light)));
   unsigned gc = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
@@ -478,9 +479,10 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
         ++c->launches, k_block<false, false><<<gbc, kBlockThreads, 0, st>>>(A, rowbuf, nrows, nullptr, 0, SortJobs{});
     } else {
       constexpr int MB = HRG_LIGHT_MINBLOCKS;
-      if (sample_ids && shard_slots)
-        ++c->launches, k_light<true, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
-      else if (shard_slots) ++c->launches, k_light<false, kSegCapShard, MB><<<gq, kLightThreads, 0, st>>>(A);
+      if (sample_ids && steep)
+        ++c->launches, k_light<true, kSegCapSteep, kSteepMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
+      else if (steep)
+        ++c->launches, k_light<false, kSegCapSteep, kSteepMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
       else if (sample_ids && !wide) ++c->launches, k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (!wide) ++c->launches, k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (sample_ids) ++c->launches, k_light<true, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);

@@ -1283,10 +1283,16 @@ constexpr float kPredErrF = 0x1.000008p-45f;  // e, rounded up
 #endif
 constexpr int kSegCapWide = HRG_WIDE_CAP;   // static shared memory stays under 48 KB
 constexpr int kWideMinBlocks = HRG_WIDE_MINB;
-#ifndef HRG_SEGCAP_SHARD
-#define HRG_SEGCAP_SHARD 16
+#ifndef HRG_SEGCAP_STEEP
+#define HRG_SEGCAP_STEEP 12
 #endif
-constexpr int kSegCapShard = HRG_SEGCAP_SHARD;  // sharded runs (few tiles per warp)
+#ifndef HRG_STEEP_MINB
+#define HRG_STEEP_MINB 8
+#endif
+// steep degree distributions (alpha >= 0.95, i.e. gamma >= 2.9): queries reach
+// fewer bands, so 12 slots defer few of them and an eighth block fits
+constexpr int kSegCapSteep = HRG_SEGCAP_STEEP;
+constexpr int kSteepMinBlocks = HRG_STEEP_MINB;
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
 struct LightSmem {
