@@ -15,6 +15,9 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <string>
 #include <thread>
 #include <vector>
@@ -1196,21 +1199,24 @@ namespace {
 // widening trails the copy by one chunk).
 constexpr size_t kWidenChunk = (size_t)1 << 24;  // ids per staged chunk (64 MB)
 #ifndef HRG_PINNED_DEVICE_FRAC
-#define HRG_PINNED_DEVICE_FRAC 0.45
+#define HRG_PINNED_DEVICE_FRAC 0.1
 #endif
 constexpr double kPinnedDeviceFrac = HRG_PINNED_DEVICE_FRAC;
 
 // Measured (config 2, 3.2e8 ids, 16 host cores): into PAGEABLE memory the
 // host widening takes 51 ms against 157 ms for the int64 copy (which stages
 // through the driver's bounce buffers).  Into PINNED memory the PCIe link and
-// the host's memory bandwidth are both busy, so the ids are split: the first
-// fraction f is widened on the device and copied as int64, the rest crosses
-// as int32 and is widened by the host threads while the copies run (PCIe
-// bytes 4 (1 + f) per id, host widening (1 - f) of the ids; f balances the
-// two).  Measured (tools/e2e_ab.py, bench.py's two-context e2e): f = 1 (one
-// int64 copy) 53.0 ms/step, 0.6 48.4, 0.45 47.5, 0.35 48.5, 0 49.6 -- the
-// host's memory bandwidth, shared by the DMA and the widening, not PCIe,
-// limits the gain.  HRG_WIDEN_DEVICE_FRAC overrides f.
+// the host's memory bandwidth are both busy, so the ids can be split: the
+// first fraction f is widened on the device and copied as int64, the rest
+// crosses as int32 and is widened by the host threads while the copies run
+// (PCIe bytes 4 (1 + f) per id, host widening (1 - f) of the ids).  With the
+// host widening writing through non-temporal stores (widen_ids: 12 instead of
+// 20 bytes of memory traffic per id) the host keeps up with most of the link
+// (tools/e2e_copy_ab.py, libraries alternating, 3 rounds, ms per copy:
+// f = 1: 51, 0.6: 46, 0.45: 45, 0.3: 45, 0.15: 42, 0: 40; with plain stores
+// 51 / 48 / 50 / 47 / 51 / 53; the two-context e2e of bench.py: 42-43 ms/step
+// at f <= 0.25 against 48-49 at 0.45).  Times vary by +-10% between runs and
+// boxes; HRG_WIDEN_DEVICE_FRAC overrides f.
 double device_widen_frac(const hrg_context* c, const void* dst) {
   if (const char* e = getenv("HRG_WIDEN_DEVICE_FRAC")) return std::min(1.0, std::max(0.0, atof(e)));
   if ((size_t)c->nnz < ((size_t)1 << 22)) return 1.0;
@@ -1220,6 +1226,26 @@ double device_widen_frac(const hrg_context* c, const void* dst) {
     return 0.0;
   }
   return at.type == cudaMemoryTypeUnregistered ? 0.0 : kPinnedDeviceFrac;
+}
+
+// int32 -> int64 of n non-negative ids on the host.  The destination is
+// written once and not read back here, so it is written with non-temporal
+// stores: a plain store first reads its cache line for ownership, and the
+// result copy is bound by the host's memory bandwidth (4 B read + 8 B written
+// per id instead of 4 + 8 + 8).
+void widen_ids(const int32_t* src, int64_t* dst, size_t n) {
+  size_t i = 0;
+#if defined(__SSE2__)
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15u)) { dst[i] = src[i]; ++i; }
+  const __m128i zero = _mm_setzero_si128();
+  for (; i + 4 <= n; i += 4) {
+    const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_unpacklo_epi32(x, zero));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 2), _mm_unpackhi_epi32(x, zero));
+  }
+  _mm_sfence();
+#endif
+  for (; i < n; ++i) dst[i] = src[i];
 }
 
 // ids [0, first) widened on the device and copied as int64; ids [first, nnz)
@@ -1261,9 +1287,7 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first) {
       if (cudaEventSynchronize(c->h_ev[ch]) != cudaSuccess) { err = 1; return; }
       const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
       const size_t lo = a + (b - a) * t / T, hi = a + (b - a) * (t + 1) / T;
-      const int32_t* src = c->h_stage;
-      int64_t* out = dst + first;
-      for (size_t i = lo; i < hi; ++i) out[i] = src[i];
+      widen_ids(c->h_stage + lo, dst + first + lo, hi - lo);
     }
   };
   if (nch > 0) {
