@@ -1197,7 +1197,9 @@ namespace {
 // and the host threads widen each chunk into the caller's array as soon as
 // its copy has landed (every thread takes a slice of every chunk, so the
 // widening trails the copy by one chunk).
-constexpr size_t kWidenChunk = (size_t)1 << 24;  // ids per staged chunk (64 MB)
+// ids per staged chunk (64 MB; 16 MB chunks or spinning on the chunk events
+// instead of blocking measured the same 38 ms per copy, 4 MB chunks 48 ms)
+constexpr size_t kWidenChunk = (size_t)1 << 24;
 #ifndef HRG_PINNED_DEVICE_FRAC
 #define HRG_PINNED_DEVICE_FRAC 0.1
 #endif

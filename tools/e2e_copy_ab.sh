@@ -1,1 +1,5 @@
-for rep in 1 2 3; do for lib in exp/lib_plain.so ""; do HRGEN_B200_LIB=$lib python tools/e2e_copy_ab.py 1 0.6 0.45 0.3 0.15 0; done; done
+# result-copy variants, libraries alternating: usage e2e_copy_ab.sh "f f f" lib lib ...
+fr=$1; shift
+for rep in 1 2 3; do for lib in "$@"; do
+  if [ "$lib" = "default" ]; then l=""; else l="exp/lib_$lib.so"; fi
+  HRGEN_B200_LIB=$l python tools/e2e_copy_ab.py $fr; done; done
