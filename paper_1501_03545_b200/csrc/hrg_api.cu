@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #if defined(__SSE2__)
 #include <emmintrin.h>
 #endif
@@ -117,7 +118,7 @@ struct hrg_context {
   int64_t launches = 0;  // this library's kernel launches (CUB's not included)
   int trig = kTrigLibm;  // sin/cos of the Poincare coordinates (hrg_context_set_trig)
   int grid_block_count = 0, grid_block_write = 0;
-  int grid_light = 0, grid_light_wide = 0, grid_light_steep = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
+  int grid_light = 0, grid_light_wide = 0, grid_heavy = 0, grid_compact = 0, grid_compact_heavy = 0;
 };
 
 namespace {
@@ -376,8 +377,6 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
 #endif
     c->grid_light = occupancy_grid(c, k_light<true, kSegCap, HRG_LIGHT_MINBLOCKS>, kLightThreads);
     c->grid_light_wide = occupancy_grid(c, k_light<true, kSegCapWide, kWideMinBlocks>, kLightThreads);
-    c->grid_light_steep =
-        occupancy_grid(c, k_light<true, kSegCapSteep, kSteepMinBlocks>, kLightThreads);
     c->grid_heavy = occupancy_grid(c, k_heavy<true>);
     c->grid_compact_heavy = occupancy_grid(c, k_compact_heavy);
 #ifdef HRG_COMPACT_CARVEOUT
@@ -417,15 +416,9 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
     wide = populated >= kWideBands;
     if (const char* e = getenv("HRG_LIGHT_WIDE")) wide = atoi(e) != 0;
   }
-  // steep degree distributions: fewer slots, one more resident block
-  // (measured at k = 4 / 16 / 64, gamma = 3: light pass -4..-6%; at
-  // gamma = 2.5 the extra deferrals cost more than the light pass gains)
-  bool steep = !wide && M->alpha >= 0.95;
-  if (const char* e = getenv("HRG_LIGHT_STEEP")) steep = !wide && atoi(e) != 0;
   unsigned gq = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kLightThreads),
-                           wide ? c->grid_light_wide
-                                : (steep ? c->grid_light_steep : c->grid_light)));
+                           wide ? c->grid_light_wide : c->grid_light));
   unsigned gc = (unsigned)std::max<int64_t>(
       1, std::min<int64_t>(blocks_for(np, kCompactThreads), c->grid_compact));
   // staging capacity: the previous call's use on this context, else a
@@ -482,11 +475,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
         ++c->launches, k_block<false, false><<<gbc, kBlockThreads, 0, st>>>(A, rowbuf, nrows, nullptr, 0, SortJobs{});
     } else {
       constexpr int MB = HRG_LIGHT_MINBLOCKS;
-      if (sample_ids && steep)
-        ++c->launches, k_light<true, kSegCapSteep, kSteepMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
-      else if (steep)
-        ++c->launches, k_light<false, kSegCapSteep, kSteepMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
-      else if (sample_ids && !wide) ++c->launches, k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
+      if (sample_ids && !wide) ++c->launches, k_light<true, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (!wide) ++c->launches, k_light<false, kSegCap, MB><<<gq, kLightThreads, 0, st>>>(A);
       else if (sample_ids) ++c->launches, k_light<true, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
       else ++c->launches, k_light<false, kSegCapWide, kWideMinBlocks><<<gq, kLightThreads, 0, st>>>(A);
@@ -1219,7 +1208,18 @@ constexpr double kPinnedDeviceFrac = HRG_PINNED_DEVICE_FRAC;
 // 51 / 48 / 50 / 47 / 51 / 53; the two-context e2e of bench.py: 42-43 ms/step
 // at f <= 0.25 against 48-49 at 0.45).  Times vary by +-10% between runs and
 // boxes; HRG_WIDEN_DEVICE_FRAC overrides f.
-double device_widen_frac(const hrg_context* c, const void* dst) {
+// The balance between the two paths is the host's (its memory bandwidth and
+// what else runs on it) against the link's, and differs between machines
+// (one all-host widening copy: 38 ms on one box of this pool, 73 ms on another,
+// where the plain int64 copy's 51 ms wins).  So the share adapts, in steps of
+// 10%, from what each split copy observed: the host threads done well before
+// the DMA -> more for the host; the host threads never waiting for a chunk
+// and finishing last -> more for the device.  Process-wide, pinned
+// destinations only; HRG_WIDEN_DEVICE_FRAC pins it.
+std::atomic<int> g_widen_pct{(int)(kPinnedDeviceFrac * 100.0 + 0.5)};
+
+double device_widen_frac(const hrg_context* c, const void* dst, bool* adaptive = nullptr) {
+  if (adaptive) *adaptive = false;
   if (const char* e = getenv("HRG_WIDEN_DEVICE_FRAC")) return std::min(1.0, std::max(0.0, atof(e)));
   if ((size_t)c->nnz < ((size_t)1 << 22)) return 1.0;
   cudaPointerAttributes at;
@@ -1227,7 +1227,9 @@ double device_widen_frac(const hrg_context* c, const void* dst) {
     cudaGetLastError();  // clear the query's error
     return 0.0;
   }
-  return at.type == cudaMemoryTypeUnregistered ? 0.0 : kPinnedDeviceFrac;
+  if (at.type == cudaMemoryTypeUnregistered) return 0.0;
+  if (adaptive) *adaptive = true;
+  return g_widen_pct.load() / 100.0;
 }
 
 // int32 -> int64 of n non-negative ids on the host.  The destination is
@@ -1252,7 +1254,7 @@ void widen_ids(const int32_t* src, int64_t* dst, size_t n) {
 
 // ids [0, first) widened on the device and copied as int64; ids [first, nnz)
 // copied as int32 in chunks and widened by the host threads as each lands.
-hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first) {
+hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool adaptive) {
   const size_t nnz = (size_t)c->nnz;
   cudaStream_t st = c->stream;
   const size_t nh = nnz - first;
@@ -1284,9 +1286,14 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first) {
     CUDA_TRY(cudaMemcpyAsync(dst, c->widen.p, 8 * first, cudaMemcpyDeviceToHost, st));
   const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::atomic<int> err{0};
+  using clk = std::chrono::steady_clock;
+  const clk::time_point t0 = clk::now();
+  double waited = 0.0;  // thread 0: seconds blocked on chunks after the first
   auto work = [&](unsigned t) {
     for (size_t ch = 0; ch < nch; ++ch) {
+      const clk::time_point w0 = clk::now();
       if (cudaEventSynchronize(c->h_ev[ch]) != cudaSuccess) { err = 1; return; }
+      if (t == 0 && ch > 0) waited += std::chrono::duration<double>(clk::now() - w0).count();
       const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
       const size_t lo = a + (b - a) * t / T, hi = a + (b - a) * (t + 1) / T;
       widen_ids(c->h_stage + lo, dst + first + lo, hi - lo);
@@ -1299,6 +1306,19 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first) {
     for (auto& th : pool) th.join();
   }
   if (err) return fail(HRG_ERR_CUDA, "index copy failed");
+  if (adaptive && nch > 1) {
+    const double t_host = std::chrono::duration<double>(clk::now() - t0).count();
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const double t_all = std::chrono::duration<double>(clk::now() - t0).count();
+    int pct = g_widen_pct.load();
+    if (t_all - t_host > 0.08 * t_all) pct -= 10;        // the DMA finished last
+    else if (waited < 0.05 * t_host) pct += 10;           // the host never waited and finished last
+    g_widen_pct.store(std::min(90, std::max(0, pct)));
+    if (getenv("HRG_WIDEN_TRACE"))
+      fprintf(stderr, "[hrg] result copy: device share %d%% host %.1f ms (waited %.1f) all %.1f ms -> %d%%\n",
+              (int)(100.0 * (double)first / (double)nnz + 0.5), 1e3 * t_host, 1e3 * waited, 1e3 * t_all,
+              g_widen_pct.load());
+  }
   return HRG_OK;
 }
 
@@ -1329,8 +1349,9 @@ hrg_status hrg_copy_result(hrg_context* c, int mem_kind, double* phi, double* rn
     if (index_bytes == 4) {
       CUDA_TRY(cudaMemcpyAsync(indices, c->idx_final, 4 * (size_t)c->nnz, k, st));
     } else if (mem_kind == HRG_MEM_HOST && device_widen_frac(c, indices) < 1.0) {
-      const size_t first = (size_t)(device_widen_frac(c, indices) * (double)c->nnz);
-      hrg_status ws = copy_indices_split(c, static_cast<int64_t*>(indices), first);
+      bool adaptive = false;
+      const size_t first = (size_t)(device_widen_frac(c, indices, &adaptive) * (double)c->nnz);
+      hrg_status ws = copy_indices_split(c, static_cast<int64_t*>(indices), first, adaptive);
       if (ws != HRG_OK) return ws;
     } else {
       // widen on the device in one pass, then one copy: the copy engine then

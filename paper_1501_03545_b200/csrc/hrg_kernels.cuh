@@ -67,6 +67,12 @@ namespace hrg {
 #ifndef HRG_DENSE_MAX
 #define HRG_DENSE_MAX 8
 #endif
+#ifndef HRG_DENSE_BIG
+#define HRG_DENSE_BIG 48
+#endif
+#ifndef HRG_DENSE_RATIO
+#define HRG_DENSE_RATIO 0.25f
+#endif
 #ifndef HRG_MID_SHIFT
 #define HRG_MID_SHIFT -1
 #endif
@@ -77,7 +83,7 @@ namespace hrg {
 #define HRG_COMPACT_MINB 5
 #endif
 #ifndef HRG_SEGCAP
-#define HRG_SEGCAP 16
+#define HRG_SEGCAP 12
 #endif
 #ifndef HRG_LIGHT_MAX
 #define HRG_LIGHT_MAX 2048
@@ -101,7 +107,7 @@ namespace hrg {
 #define HRG_HEAVY_BATCH 4
 #endif
 #ifndef HRG_LIGHT_MINBLOCKS
-#define HRG_LIGHT_MINBLOCKS 7
+#define HRG_LIGHT_MINBLOCKS 8
 #endif
 
 constexpr int kMaxBands = 32;     // one warp lane per radial band
@@ -1193,6 +1199,8 @@ constexpr int kBandGroup = HRG_BAND_GROUP;    // bands resolved together (loads 
 constexpr bool kTrimUnion = HRG_TRIM_UNION;   // ... and of the tile's union windows
 constexpr int kUnionSmall = HRG_UNION_SMALL;  // union windows this small are shared by the tile
 constexpr int kDenseMax = HRG_DENSE_MAX;      // ... and up to this size tested as a dense block
+constexpr int kDenseBig = HRG_DENSE_BIG;      // ... or up to this size if the windows cover
+constexpr float kDenseRatio = HRG_DENSE_RATIO;  //     this fraction of the union
 constexpr int kDenseCap = 64;                 // dense candidates per tile (one bit each)
 constexpr int kShareSlack = HRG_SHARE_SLACK;  // (experiment) union shared if it exceeds the
                                               // tile's narrowest window by at most this
@@ -1283,16 +1291,6 @@ constexpr float kPredErrF = 0x1.000008p-45f;  // e, rounded up
 #endif
 constexpr int kSegCapWide = HRG_WIDE_CAP;   // static shared memory stays under 48 KB
 constexpr int kWideMinBlocks = HRG_WIDE_MINB;
-#ifndef HRG_SEGCAP_STEEP
-#define HRG_SEGCAP_STEEP 12
-#endif
-#ifndef HRG_STEEP_MINB
-#define HRG_STEEP_MINB 8
-#endif
-// steep degree distributions (alpha >= 0.95, i.e. gamma >= 2.9): queries reach
-// fewer bands, so 12 slots defer few of them and an eighth block fits
-constexpr int kSegCapSteep = HRG_SEGCAP_STEEP;
-constexpr int kSteepMinBlocks = HRG_STEEP_MINB;
 constexpr int kWideBands = 26;   // populated bands from which the wide variant is used
 template <int kCap>
 struct LightSmem {
@@ -1379,6 +1377,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     unsigned cheap = 0, dense = 0, skip = 0;
     int32_t uA = 0, uAe = 0, uB = 0, uBe = 0;
     int32_t dex = 0, Dn = 0;  // lane = band: first dense-list index of its candidates; their total
+    bool dense_big = false;  // a larger union of which every query needs a good part
     {
       double pmin = active ? phi : 1e300, pmax = active ? phi : -1e300;
       float rmin = rvq, rmax = active ? rvq : 0.0f;
@@ -1414,10 +1413,15 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         const float nb = (float)(sb[lane].end - sb[lane].start);
         const float w_est = dn < 0.0f ? 0.0f : (dn >= 3.14159265f ? nb : dn * nb * 0.31830988f);
         if (un <= kUnionSmall || (float)un <= w_est + (float)kShareSlack) cheap = 1;
+        // a dense test costs ~0.65 instructions per pair against ~3 in the
+        // walk (plus the window and flatten work of a segment), so a union of
+        // up to kDenseBig candidates is also tested densely when the tile's
+        // narrowest window covers at least kDenseRatio of it
+        dense_big = kDenseBig > 0 && un <= kDenseBig && w_est >= kDenseRatio * (float)un;
       }
       cheap = __ballot_sync(FULL, cheap != 0);
       skip = __ballot_sync(FULL, un == 0 || lane >= A.L);
-      bool dn_ok = kDenseMax > 0 && un > 0 && un <= kDenseMax;
+      bool dn_ok = kDenseMax > 0 && un > 0 && (un <= kDenseMax || dense_big);
       if (!kSampleIds) {
         // positions are ids and rows leave sorted: dense hits are written
         // ahead of a row's walked hits, so dense bands must lie inside every

@@ -219,16 +219,13 @@ def test_generate_matches_oracle(oracle, kw):
           f"CR-vs-libm trig pairs={d['only_got'] + d['only_want']} max_gap={d['max_gap']:.3g}")
 
 
-@pytest.mark.parametrize("variant", ["wide0-steep0", "wide0-steep1", "wide1"])
+@pytest.mark.parametrize("wide", ["0", "1"])
 @pytest.mark.parametrize("kw", [GEN_CASES[1], GEN_CASES[2], GEN_CASES[5]],
                          ids=["k32-g2.5", "k4-g2.2", "R35.5"])
-def test_light_query_variants_match_oracle(oracle, kw, variant, monkeypatch):
-    """All three light-query variants (16 segment slots; 12 for steep degree
-    distributions; 36 when most bands hold points -- the model picks one,
-    HRG_LIGHT_WIDE / HRG_LIGHT_STEEP force it) give the oracle's edge set
-    exactly."""
-    monkeypatch.setenv("HRG_LIGHT_WIDE", "1" if variant == "wide1" else "0")
-    monkeypatch.setenv("HRG_LIGHT_STEEP", "1" if variant.endswith("steep1") else "0")
+def test_light_query_variants_match_oracle(oracle, kw, wide, monkeypatch):
+    """Both light-query variants (12 and 36 segment slots; the model picks
+    one, HRG_LIGHT_WIDE forces it) give the oracle's edge set exactly."""
+    monkeypatch.setenv("HRG_LIGHT_WIDE", wide)
     p = GeneratorParams(**kw)
     model = p.resolve()
     g = P.generate(p)
