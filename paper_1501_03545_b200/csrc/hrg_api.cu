@@ -1216,6 +1216,7 @@ constexpr double kPinnedDeviceFrac = HRG_PINNED_DEVICE_FRAC;
 // the DMA -> more for the host; the host threads never waiting for a chunk
 // and finishing last -> more for the device.  Process-wide, pinned
 // destinations only; HRG_WIDEN_DEVICE_FRAC pins it.
+constexpr int kWidenMaxPct = 60;  // bounds the device-side widening buffer
 std::atomic<int> g_widen_pct{(int)(kPinnedDeviceFrac * 100.0 + 0.5)};
 
 double device_widen_frac(const hrg_context* c, const void* dst, bool* adaptive = nullptr) {
@@ -1258,17 +1259,21 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool a
   const size_t nnz = (size_t)c->nnz;
   cudaStream_t st = c->stream;
   const size_t nh = nnz - first;
+  // both staging buffers are sized for any share the adaptation may pick
+  // (re-allocating a pinned gigabyte costs more than many copies)
+  const size_t wcap = adaptive ? std::max(first, (size_t)(0.01 * kWidenMaxPct * (double)nnz) + 1) : first;
+  const size_t hcap = adaptive ? nnz : nh;
   if (first > 0) {
-    CUDA_TRY(c->widen.ensure(8 * first));
+    CUDA_TRY(c->widen.ensure(8 * wcap));
     ++c->launches, k_widen<<<blocks_for((int64_t)first), 256, 0, st>>>((int64_t)first, c->idx_final,
                                                                        c->widen.as<int64_t>());
   }
-  if (c->h_stage_bytes < 4 * nh) {
+  if (c->h_stage_bytes < 4 * hcap) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     c->h_stage = nullptr;
     c->h_stage_bytes = 0;
-    CUDA_TRY(cudaMallocHost(&c->h_stage, std::max<size_t>(4 * nh, 4)));
-    c->h_stage_bytes = std::max<size_t>(4 * nh, 4);
+    CUDA_TRY(cudaMallocHost(&c->h_stage, std::max<size_t>(4 * hcap, 4)));
+    c->h_stage_bytes = std::max<size_t>(4 * hcap, 4);
   }
   const size_t nch = (nh + kWidenChunk - 1) / kWidenChunk;
   while (c->h_ev.size() < nch) {
@@ -1313,7 +1318,7 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool a
     int pct = g_widen_pct.load();
     if (t_all - t_host > 0.08 * t_all) pct -= 10;        // the DMA finished last
     else if (waited < 0.05 * t_host) pct += 10;           // the host never waited and finished last
-    g_widen_pct.store(std::min(90, std::max(0, pct)));
+    g_widen_pct.store(std::min(kWidenMaxPct, std::max(0, pct)));
     if (getenv("HRG_WIDEN_TRACE"))
       fprintf(stderr, "[hrg] result copy: device share %d%% host %.1f ms (waited %.1f) all %.1f ms -> %d%%\n",
               (int)(100.0 * (double)first / (double)nnz + 0.5), 1e3 * t_host, 1e3 * waited, 1e3 * t_all,
