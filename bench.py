@@ -390,10 +390,11 @@ def run_ours(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * float(dt.item()),
                "ms_per_step_one_context": 1e3 * seq,
                "api": "hrg_generate + hrg_copy_result (C ABI) into pinned host buffers, "
-                      "int64 CSR (10% of the ids widened on the device and copied as int64, "
-                      "the rest cross PCIe as int32 and are widened into the caller's array "
-                      "by host threads, with non-temporal stores, while the copies run; "
-                      "d2h_bytes_per_step counts the int64 result); two contexts on two streams alternating steps (the copy "
+                      "int64 CSR (an adaptive 0-60% share of the ids is widened on the device "
+                      "and copied as int64, the rest cross PCIe as int32 -- 3 bytes each when "
+                      "n <= 2^24 -- and are widened into the caller's array by host threads, "
+                      "with non-temporal stores, while the copies run; d2h_bytes_per_step "
+                      "counts the int64 result); two contexts on two streams alternating steps (the copy "
                       "of one graph overlaps the generation of the next); inputs are 5 "
                       "scalar parameters"}
         del engines

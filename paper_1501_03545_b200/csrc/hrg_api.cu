@@ -19,6 +19,9 @@
 #if defined(__SSE2__)
 #include <emmintrin.h>
 #endif
+#if defined(__x86_64__)
+#include <tmmintrin.h>
+#endif
 #include <string>
 #include <thread>
 #include <vector>
@@ -95,7 +98,7 @@ struct hrg_context {
   int64_t nq = 0;
   Buf temp, k32_in, k32_out, sh_buf, sh_bands, sh_wtab, sh_keep, sh_gid;
   bool sh_sampled = false;  // sharded sampling: vals are compact indices, sh_gid the ids
-  Buf widen;
+  Buf widen, pack;
   int32_t* h_stage = nullptr;      // pinned int32 staging of the indices (host widening)
   size_t h_stage_bytes = 0;
   std::vector<cudaEvent_t> h_ev;   // one per staged chunk
@@ -924,7 +927,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
                  &c->chunk_row, &c->tv0, &c->wtab, &c->job_dst, &c->job_len,
                  &c->mid_off, &c->mid_len, &c->bands, &c->dir, &c->dir_total, &c->bad, &c->dir_gaps, &c->band_pmin,
                  &c->deg, &c->rowptr, &c->idx, &c->cand, &c->rowidx, &c->row_ids, &c->rowptr_c, &c->nq_buf, &c->temp, &c->k32_in, &c->k32_out, &c->sh_buf, &c->sh_bands, &c->sh_wtab, &c->sh_keep, &c->sh_gid,
-                 &c->widen})
+                 &c->widen, &c->pack})
     b->release();
   if (c->h_rb) cudaFreeHost(c->h_rb);
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -1253,8 +1256,44 @@ void widen_ids(const int32_t* src, int64_t* dst, size_t n) {
   for (; i < n; ++i) dst[i] = src[i];
 }
 
+// 3-byte ids (k_pack3) -> int64, the same way.  src + 3 n may be read up to
+// 16 bytes past the last id's bytes only where the caller's buffer has them
+// (the last 8 ids are unpacked byte by byte).
+#if defined(__x86_64__)
+__attribute__((target("ssse3")))
+#endif
+void widen_ids3(const uint8_t* src, int64_t* dst, size_t n) {
+  size_t i = 0;
+  auto one = [&](size_t k) {
+    dst[k] = (int64_t)src[3 * k] | ((int64_t)src[3 * k + 1] << 8) | ((int64_t)src[3 * k + 2] << 16);
+  };
+#if defined(__x86_64__)
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15u)) { one(i); ++i; }
+  const __m128i lo = _mm_setr_epi8(0, 1, 2, -1, -1, -1, -1, -1, 3, 4, 5, -1, -1, -1, -1, -1);
+  const __m128i hi = _mm_setr_epi8(6, 7, 8, -1, -1, -1, -1, -1, 9, 10, 11, -1, -1, -1, -1, -1);
+  for (; i + 12 <= n; i += 4) {  // 16 bytes loaded, 12 used: stay 8 ids inside the slice
+    const __m128i x = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 3 * i));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), _mm_shuffle_epi8(x, lo));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 2), _mm_shuffle_epi8(x, hi));
+  }
+  _mm_sfence();
+#endif
+  for (; i < n; ++i) one(i);
+}
+
+bool use_pack3(const hrg_context* c) {
+  if (c->n > ((int64_t)1 << 24)) return false;
+  if (const char* e = getenv("HRG_PACK3")) return atoi(e) != 0;
+#if defined(__x86_64__)
+  return __builtin_cpu_supports("ssse3");
+#else
+  return false;
+#endif
+}
+
 // ids [0, first) widened on the device and copied as int64; ids [first, nnz)
-// copied as int32 in chunks and widened by the host threads as each lands.
+// copied as int32 -- or, when every id fits 24 bits, as 3 bytes each -- in
+// chunks and widened by the host threads as each lands.
 hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool adaptive) {
   const size_t nnz = (size_t)c->nnz;
   cudaStream_t st = c->stream;
@@ -1281,10 +1320,21 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool a
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
     c->h_ev.push_back(e);
   }
+  const bool pack3 = use_pack3(c) && nh >= 64;
+  uint8_t* const h_bytes = reinterpret_cast<uint8_t*>(c->h_stage);
+  if (pack3) {
+    CUDA_TRY(c->pack.ensure(3 * (adaptive ? nnz : nh) + 64));
+    ++c->launches, k_pack3<<<blocks_for((int64_t)((nh + 3) / 4)), 256, 0, st>>>(
+        (int64_t)nh, c->idx_final + first, c->pack.as<uint32_t>());
+  }
   for (size_t ch = 0; ch < nch; ++ch) {
     const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
-    CUDA_TRY(cudaMemcpyAsync(c->h_stage + a, c->idx_final + first + a, 4 * (b - a),
-                             cudaMemcpyDeviceToHost, st));
+    if (pack3)
+      CUDA_TRY(cudaMemcpyAsync(h_bytes + 3 * a, c->pack.as<uint8_t>() + 3 * a, 3 * (b - a),
+                               cudaMemcpyDeviceToHost, st));
+    else
+      CUDA_TRY(cudaMemcpyAsync(c->h_stage + a, c->idx_final + first + a, 4 * (b - a),
+                               cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(c->h_ev[ch], st));
   }
   if (first > 0)
@@ -1301,7 +1351,8 @@ hrg_status copy_indices_split(hrg_context* c, int64_t* dst, size_t first, bool a
       if (t == 0 && ch > 0) waited += std::chrono::duration<double>(clk::now() - w0).count();
       const size_t a = ch * kWidenChunk, b = std::min(nh, a + kWidenChunk);
       const size_t lo = a + (b - a) * t / T, hi = a + (b - a) * (t + 1) / T;
-      widen_ids(c->h_stage + lo, dst + first + lo, hi - lo);
+      if (pack3) widen_ids3(h_bytes + 3 * lo, dst + first + lo, hi - lo);
+      else widen_ids(c->h_stage + lo, dst + first + lo, hi - lo);
     }
   };
   if (nch > 0) {

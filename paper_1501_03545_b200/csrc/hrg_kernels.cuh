@@ -3055,6 +3055,22 @@ __global__ void __launch_bounds__(256) k_expand_rows(int64_t nq, const int64_t* 
   }
 }
 
+// Ids below 2^24 as 3 little-endian bytes each (the result copy's transfer
+// format when n <= 2^24): a thread packs 4 ids into 3 words.  `in` need not
+// be 16-byte aligned (it starts anywhere in the index array).
+__global__ void __launch_bounds__(256) k_pack3(int64_t n, const int32_t* __restrict__ in,
+                                               uint32_t* __restrict__ out) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t i = 4 * g;
+  if (i >= n) return;
+  uint32_t x[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) x[t] = i + t < n ? (uint32_t)in[i + t] & 0xffffffu : 0u;
+  out[3 * g] = x[0] | (x[1] << 24);
+  out[3 * g + 1] = (x[1] >> 8) | (x[2] << 16);
+  out[3 * g + 2] = (x[2] >> 16) | (x[3] << 8);
+}
+
 __global__ void __launch_bounds__(256) k_widen(int64_t n, const int32_t* __restrict__ in,
                                                int64_t* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -255,6 +255,33 @@ def test_tile_order_and_dense_block_match_oracle(oracle, mix, order, monkeypatch
     assert g.m == m and np.array_equal(g.edge_array(), e)
 
 
+def test_result_copy_paths_agree(monkeypatch):
+    """hrg_copy_result's int64 index copy into host memory has several paths
+    (ids widened on the device; crossing PCIe as int32 or, for n <= 2^24, as
+    3-byte ids and widened by host threads with non-temporal stores; any split
+    between the two; pinned or pageable destination).  All give the int32 copy
+    widened by numpy."""
+    p = GeneratorParams(n=1_500_000, avg_degree=12.0, gamma=2.8, seed=21)
+    eng = P.get_engine()
+    eng.generate(p.resolve(), p.seed, P.generator.VERTEX_ORDERS[p.vertex_order])
+    ip32, ix32 = eng.copy_csr(np.int32, pinned=False)
+    assert ix32.size >= 1 << 22  # large enough for the split paths
+    want = ix32.astype(np.int64)
+    for frac in ("0", "0.3", "0.97", "1"):
+        for pack in ("0", "1"):
+            for pinned in (True, False):
+                monkeypatch.setenv("HRG_WIDEN_DEVICE_FRAC", frac)
+                monkeypatch.setenv("HRG_PACK3", pack)
+                ip, ix = eng.copy_csr(np.int64, pinned=pinned)
+                assert np.array_equal(ix, want), (frac, pack, pinned)
+                assert np.array_equal(ip, ip32)
+    monkeypatch.delenv("HRG_WIDEN_DEVICE_FRAC")
+    monkeypatch.delenv("HRG_PACK3")
+    for _ in range(4):  # the adaptive share
+        ip, ix = eng.copy_csr(np.int64, pinned=True)
+        assert np.array_equal(ix, want)
+
+
 def test_config1_full_size_matches_oracle(oracle):
     """BASELINE config 1 (n=1e6, k=10, gamma=3, seed 1) end to end."""
     p = GeneratorParams(n=1_000_000, avg_degree=10.0, gamma=3.0, seed=1)
