@@ -58,9 +58,6 @@ namespace hrg {
 #ifndef HRG_DIR_EXTRA
 #define HRG_DIR_EXTRA 1
 #endif
-#ifndef HRG_SHARE_SLACK
-#define HRG_SHARE_SLACK -100000
-#endif
 #ifndef HRG_UNION_SMALL
 #define HRG_UNION_SMALL 2
 #endif
@@ -1085,48 +1082,6 @@ __device__ __forceinline__ QFull load_query(const QueryArgs& A, int32_t v) {
   return f;
 }
 
-// One candidate's data for its pair test: the circle of w if w's id is the
-// smaller (it decides), else the point of w.
-struct Cand {
-  double d0, d1, d2;
-  int32_t id;
-  bool lower;
-};
-
-template <bool kSampleIds>
-__device__ __forceinline__ Cand load_cand(const QueryArgs& A, const QFull& f, int32_t w) {
-  Cand c;
-  if (kSampleIds) {
-    double2 a, b, x;
-    load_rec(A.rec, w, a, b, x);
-    c.id = (int32_t)(__double_as_longlong(x.y) & 0xffffffffll);
-    c.lower = c.id < f.idv;
-    c.d0 = c.lower ? b.x : a.x;
-    c.d1 = c.lower ? b.y : a.y;
-    c.d2 = x.x;
-  } else {
-    c.id = w;
-    c.lower = w < f.pos;  // angular ids are positions
-    if (c.lower) {
-      const Circ ci = load_circ(A.rec, w);
-      c.d0 = ci.cx; c.d1 = ci.cy; c.d2 = ci.rsq;
-    } else {
-      const double2 p = load_pt(A.rec, w);
-      c.d0 = p.x; c.d1 = p.y; c.d2 = 0.0;
-    }
-  }
-  return c;
-}
-
-// Edge {v, w} is decided by the circle of the smaller vertex id, exactly as
-// hrgen queries from v and keeps ids > v (generator.py:182-187).
-__device__ __forceinline__ bool pair_test(const QFull& f, const Cand& c, int32_t w) {
-  const double x = c.lower ? f.px : c.d0, y = c.lower ? f.py : c.d1;  // pred(w -> v) :
-  const double cx = c.lower ? c.d0 : f.cx, cy = c.lower ? c.d1 : f.cy;  // pred(v -> w)
-  const double rs = c.lower ? c.d2 : f.rsq;
-  return ref_pred(x, y, cx, cy, rs) && w != f.pos;
-}
-
 __device__ __forceinline__ void load_bands(const QueryArgs& A, Band* sb) {
   if (threadIdx.x < A.L) sb[threadIdx.x] = A.bands[threadIdx.x];
   __syncthreads();
@@ -1202,8 +1157,6 @@ constexpr int kDenseMax = HRG_DENSE_MAX;      // ... and up to this size tested 
 constexpr int kDenseBig = HRG_DENSE_BIG;      // ... or up to this size if the windows cover
 constexpr float kDenseRatio = HRG_DENSE_RATIO;  //     this fraction of the union
 constexpr int kDenseCap = 64;                 // dense candidates per tile (one bit each)
-constexpr int kShareSlack = HRG_SHARE_SLACK;  // (experiment) union shared if it exceeds the
-                                              // tile's narrowest window by at most this
 
 // Walk-step candidate data, loaded before the query's side is known in
 // sample order (the full record), or by the query's position in angular
@@ -1406,13 +1359,11 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
         if (r.eB < r.sB) r.eB = r.sB;
         uA = r.sA; uAe = r.eA; uB = r.sB; uBe = r.eB;
         un = (uAe - uA) + (uBe - uB);
-        // the narrowest window of the tile (its outermost query), in points:
-        // if the union exceeds it by little, testing the union costs fewer
-        // instructions than resolving 32 windows
+        // the narrowest window of the tile (its outermost query), in points
         const float dn = __ldg(wtab_row(A, rmax) + lane);
         const float nb = (float)(sb[lane].end - sb[lane].start);
         const float w_est = dn < 0.0f ? 0.0f : (dn >= 3.14159265f ? nb : dn * nb * 0.31830988f);
-        if (un <= kUnionSmall || (float)un <= w_est + (float)kShareSlack) cheap = 1;
+        if (un <= kUnionSmall) cheap = 1;
         // a dense test costs ~0.65 instructions per pair against ~3 in the
         // walk (plus the window and flatten work of a segment), so a union of
         // up to kDenseBig candidates is also tested densely when the tile's
