@@ -1678,8 +1678,13 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
       __syncwarp();
       const int32_t row0 = mine + dhi - dh;  // the row's first slot in the tile's range
       sm.hits[tid] = end - mine + dh;
-      for (unsigned long long m = dm; m; m &= m - 1)
-        out[row0 + __popcll(dm & ((m & -m) - 1))] = sm.dids[tid >> 5][__ffsll((long long)m) - 1];
+      {
+        // the dense hits, in candidate order (32-bit halves of the mask)
+        const int32_t* dids = sm.dids[tid >> 5];
+        int32_t at = row0;
+        for (unsigned m = (unsigned)dm; m; m &= m - 1) out[at++] = dids[__ffs(m) - 1];
+        for (unsigned m = (unsigned)(dm >> 32); m; m &= m - 1) out[at++] = dids[31 + __ffs(m)];
+      }
       if (light) {  // the row's hits: stage[stage_off, stage_off + slots)
         A.stage_off[v] = (int64_t)base + row0;
         A.slots[v] = end - mine + dh;
