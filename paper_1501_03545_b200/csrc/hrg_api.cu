@@ -84,7 +84,7 @@ struct hrg_context {
   // sort
   Buf keys_out, vals_in, vals_out;
   // sorted records
-  Buf pt, circ, rec, s_phi, s_rf, s_invd, s_rp, s_rn, pr;
+  Buf pt, circ, s_phi, s_rf, s_invd, s_rp, s_rn, pr;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits, chunk_entry,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
@@ -162,7 +162,6 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->pr.ensure(2 * d));
   CUDA_TRY(c->pt.ensure(16 * (size_t)n));
   CUDA_TRY(c->circ.ensure(sizeof(Circ) * (size_t)n));
-  CUDA_TRY(c->rec.ensure(sizeof(Rec) * (size_t)n));
   CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(128));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
   CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
@@ -225,7 +224,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                                            c->vals_out.as<int32_t>(), (int)n, 0, 32, st));
   CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
   QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_invd.as<float>()};
-  const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
+  const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(),
                   c->vals_out.as<int32_t>()};
   CUDA_TRY(c->band_pmin.ensure(8 * kMaxBands));
   unsigned long long* band_pmin = c->band_pmin.as<unsigned long long>();
@@ -301,7 +300,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   cudaStream_t st = c->stream;
   QueryArgs A;
   memset(&A, 0, sizeof(A));
-  A.rec = Recs{c->pt.as<double2>(), c->circ.as<Circ>(), c->rec.as<Rec>(),
+  A.rec = Recs{c->pt.as<double2>(), c->circ.as<Circ>(),
                 c->vals_out.as<int32_t>()};
   A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_invd.as<float>()};
   A.a = M->cosh_r_minus_1;
@@ -919,7 +918,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->pt, &c->circ, &c->rec, &c->s_phi, &c->s_rf, &c->s_invd, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
+                 &c->pt, &c->circ, &c->s_phi, &c->s_rf, &c->s_invd, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_entry, &c->chunk_off,
                  &c->slots,

@@ -75,16 +75,11 @@ struct __align__(16) QB {
 template <bool kSampleIds>
 __device__ __forceinline__ QB load_qb(const QueryArgs& A, int32_t v) {
   QB b;
-  if (kSampleIds) {
-    double2 a, c, x;
-    load_rec(A.rec, v, a, c, x);
-    b.px = a.x; b.py = a.y; b.cx = c.x; b.cy = c.y; b.rsq = x.x;
-    b.id = (int32_t)(__double_as_longlong(x.y) & 0xffffffffll);
-  } else {
+  {
     const double2 p = load_pt(A.rec, v);
     const Circ ci = load_circ(A.rec, v);
     b.px = p.x; b.py = p.y; b.cx = ci.cx; b.cy = ci.cy; b.rsq = ci.rsq;
-    b.id = v;  // angular ids are positions
+    b.id = kSampleIds ? __ldg(A.rec.ids + v) : v;  // angular ids are positions
   }
   b.pad = 0;
   return b;

@@ -8,9 +8,9 @@
 //                    k_shard_points keep only the points the sector can reach.
 //   cub radix sort   keys -> permutation into (band, angle) order.
 //   k_gather         fp64 records in sorted order: the 16-byte point (p_x, p_y)
-//                    every pair test reads, and the 48-byte full record (point,
-//                    query circle c_x, c_y, rad^2, id) of the query side and the
-//                    rare other-orientation test; glibc's sin/cos bit for bit,
+//                    every pair test reads, and the 32-byte query circle
+//                    (c_x, c_y, rad^2) of the query side and the rare
+//                    other-orientation test; glibc's sin/cos bit for bit,
 //                    hrgen's circle transform (geometry.py:141-157); per-band
 //                    innermost radius; 1/D per point (the test's margin).
 //   k_band_setup / k_dir_fill / k_dir_gaps / k_dir_tail / k_window_table /
@@ -280,27 +280,18 @@ __global__ void __launch_bounds__(256) k_keys_from_coords(int64_t n, const doubl
   vals[i] = (int32_t)i;
 }
 
-// Candidate records, split by orientation so a pair test fetches only what
-// it needs: the point (p_x, p_y) for pred(v -> w), 16 B, or the circle
-// (c_x, c_y, rad^2), 32 B, for pred(w -> v); the vertex id (4 B, the sort
-// permutation) decides which.
+// Per-point records, split so a pair test fetches only what it needs: the
+// point (p_x, p_y), 16 B, for pred(v -> w) -- every candidate -- and the circle
+// (c_x, c_y, rad^2), 32 B, for the query side and for pred(w -> v) inside the
+// rounding margin; the vertex id (4 B, the sort permutation) beside them.
 struct __align__(16) Circ {
   double cx, cy, rsq, pad;
 };
 
-// Sample-order ids: the orientation is known only once w's id is read, so
-// the whole record (both halves + id, 48 B) is fetched in one go instead.
-struct __align__(16) Rec {
-  double px, py, cx, cy, rsq;
-  int32_t id;
-  int32_t pad;
-};
-
 struct Recs {
-  double2* pt;          // angular order
-  Circ* circ;           // angular order
-  Rec* rec;             // sample order
-  const int32_t* ids;   // sorted position -> vertex id
+  double2* pt;          // the point (p_x, p_y): what a pair test reads of a candidate
+  Circ* circ;           // the query circle: the query side, and the rare other orientation
+  const int32_t* ids;   // sorted position -> vertex id (sample order)
 };
 
 struct QRec {          // query-side extras, per sorted position
@@ -375,11 +366,7 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
     const double D = a * ((1.0 - r) * (1.0 + r)) + 2.0;
     q.invd[p] = __double2float_ru(1.0 / D) * (1.0f + 0x1p-18f);
   }
-  if (kSampleIds) {
-    Rec R;
-    R.px = px; R.py = py; R.cx = cx; R.cy = cy; R.rsq = rsq; R.id = id; R.pad = 0;
-    rec.rec[p] = R;
-  } else {
+  {
     Circ ci;
     ci.cx = cx; ci.cy = cy; ci.rsq = rsq; ci.pad = 0.0;
     rec.circ[p] = ci;
@@ -1058,27 +1045,14 @@ struct QFull {
   int32_t pos, idv;
 };
 
-__device__ __forceinline__ void load_rec(const Recs& R, int32_t w, double2& a, double2& b,
-                                         double2& c) {
-  const double2* q = reinterpret_cast<const double2*>(R.rec + w);
-  a = __ldg(q); b = __ldg(q + 1); c = __ldg(q + 2);
-}
-
 template <bool kSampleIds>
 __device__ __forceinline__ QFull load_query(const QueryArgs& A, int32_t v) {
   QFull f;
   f.pos = v;
-  if (kSampleIds) {
-    double2 a, b, c;
-    load_rec(A.rec, v, a, b, c);
-    f.px = a.x; f.py = a.y; f.cx = b.x; f.cy = b.y; f.rsq = c.x;
-    f.idv = (int32_t)(__double_as_longlong(c.y) & 0xffffffffll);
-  } else {
-    const double2 p = load_pt(A.rec, v);
-    const Circ c = load_circ(A.rec, v);
-    f.px = p.x; f.py = p.y; f.cx = c.cx; f.cy = c.cy; f.rsq = c.rsq;
-    f.idv = v;
-  }
+  const double2 p = load_pt(A.rec, v);
+  const Circ c = load_circ(A.rec, v);
+  f.px = p.x; f.py = p.y; f.cx = c.cx; f.cy = c.cy; f.rsq = c.rsq;
+  f.idv = kSampleIds ? __ldg(A.rec.ids + v) : v;  // angular ids are positions
   return f;
 }
 
@@ -1158,50 +1132,6 @@ constexpr int kDenseBig = HRG_DENSE_BIG;      // ... or up to this size if the w
 constexpr float kDenseRatio = HRG_DENSE_RATIO;  //     this fraction of the union
 constexpr int kDenseCap = 64;                 // dense candidates per tile (one bit each)
 
-// Walk-step candidate data, loaded before the query's side is known in
-// sample order (the full record), or by the query's position in angular
-// order (the circle of a smaller id, else the point).
-struct LoadedCand {
-  double2 a, b;
-  double2 x;  // sample order: (rsq, id bits); angular: unused
-};
-
-template <bool kSampleIds>
-__device__ __forceinline__ LoadedCand load_walk_cand(const QueryArgs& A, int32_t qpos, int32_t w) {
-  LoadedCand c;
-  if (kSampleIds) {
-    load_rec(A.rec, w, c.a, c.b, c.x);
-  } else if (w < qpos) {
-    const double2* q = reinterpret_cast<const double2*>(A.rec.circ + w);
-    c.a = __ldg(q); c.b = __ldg(q + 1);
-  } else {
-    c.a = __ldg(A.rec.pt + w);
-  }
-  return c;
-}
-
-template <bool kSampleIds>
-__device__ __forceinline__ bool walk_test(const QFull& f, const LoadedCand& c, int32_t w,
-                                          int32_t& id) {
-  // operands selected first, one predicate evaluation (no divergent branch):
-  // lower -> pred(w -> v) with w's circle, else pred(v -> w) with v's
-  if (kSampleIds) {
-    id = (int32_t)(__double_as_longlong(c.x.y) & 0xffffffffll);
-    const bool lower = id < f.idv;
-    const double x = lower ? f.px : c.a.x, y = lower ? f.py : c.a.y;
-    const double cx = lower ? c.b.x : f.cx, cy = lower ? c.b.y : f.cy;
-    const double rs = lower ? c.x.x : f.rsq;
-    return ref_pred(x, y, cx, cy, rs) && id != f.idv;
-  } else {
-    id = w;
-    const bool lower = w < f.pos;
-    const double x = lower ? f.px : c.a.x, y = lower ? f.py : c.a.y;
-    const double cx = lower ? c.a.x : f.cx, cy = lower ? c.a.y : f.cy;
-    const double rs = lower ? c.b.x : f.rsq;
-    return ref_pred(x, y, cx, cy, rs) && w != f.pos;
-  }
-}
-
 constexpr int kWalkUnroll = HRG_WALK_UNROLL;  // walk steps whose loads are in flight together
 // flat entry, second word: flat index of the segment's first candidate
 // (16 bits) | query lane << 16 | band << 21 | the query's first segment << 31
@@ -1260,15 +1190,9 @@ struct LightSmem {
 // w's circle (c_x, c_y, rad^2), for pred(w -> v): the walk's margin case
 template <bool kSampleIds>
 __device__ __forceinline__ void load_other(const Recs& R, int32_t w, double2& cxy, double& rsq) {
-  if (kSampleIds) {
-    const Rec* r = R.rec + w;
-    cxy = __ldg(reinterpret_cast<const double2*>(&r->cx));
-    rsq = __ldg(&r->rsq);
-  } else {
-    const Circ* c = R.circ + w;
-    cxy = __ldg(reinterpret_cast<const double2*>(&c->cx));
-    rsq = __ldg(&c->rsq);
-  }
+  const Circ* c = R.circ + w;
+  cxy = __ldg(reinterpret_cast<const double2*>(&c->cx));
+  rsq = __ldg(&c->rsq);
 }
 
 template <int kCap>
