@@ -84,7 +84,7 @@ struct hrg_context {
   // sort
   Buf keys_out, vals_in, vals_out;
   // sorted records
-  Buf pt, circ, s_phi, s_rf, s_invd, s_rp, s_rn, pr;
+  Buf pt, circ, s_phi, s_rp, s_rn, pr;
   // staging + heavy queries
   Buf stage, stage_off, counters, heavy_v, heavy_c, heavy_of, nchunks, chunk_start, chunk_hits, chunk_entry,
       chunk_off, slots, large_off, large_len, giant_off, giant_len, giant_meta,
@@ -165,7 +165,6 @@ hrg_status ensure_point_buffers(hrg_context* c, int64_t n) {
   CUDA_TRY(c->stage_off.ensure(8 * (size_t)n)); CUDA_TRY(c->counters.ensure(128));
   CUDA_TRY(c->heavy_v.ensure(i32)); CUDA_TRY(c->heavy_c.ensure(i32));
   CUDA_TRY(c->heavy_of.ensure(i32)); CUDA_TRY(c->slots.ensure(i32));
-  CUDA_TRY(c->s_rf.ensure(f)); CUDA_TRY(c->s_invd.ensure(f));
   CUDA_TRY(c->bands.ensure(sizeof(Band) * kMaxBands));
   CUDA_TRY(c->dir.ensure(4 * (size_t)((2 * n << kDirExtra) + 2 * kMaxBands + 64)));
   CUDA_TRY(c->dir_total.ensure(16)); CUDA_TRY(c->bad.ensure(8)); CUDA_TRY(c->cand.ensure(8));
@@ -223,7 +222,7 @@ hrg_status build_index(hrg_context* c, const hrg_model* M, const BandSpec& S, in
                                            c->k32_out.as<uint32_t>(), c->vals_in.as<int32_t>(),
                                            c->vals_out.as<int32_t>(), (int)n, 0, 32, st));
   CUDA_TRY(cudaEventRecord(c->ev[E_SORTED], st));
-  QRec q{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_invd.as<float>()};
+  QRec q{c->s_phi.as<double>()};
   const Recs recs{c->pt.as<double2>(), c->circ.as<Circ>(),
                   c->vals_out.as<int32_t>()};
   CUDA_TRY(c->band_pmin.ensure(8 * kMaxBands));
@@ -302,7 +301,7 @@ hrg_status emit_edges(hrg_context* c, const hrg_model* M, int L, double C, bool 
   memset(&A, 0, sizeof(A));
   A.rec = Recs{c->pt.as<double2>(), c->circ.as<Circ>(),
                 c->vals_out.as<int32_t>()};
-  A.q = QRec{c->s_phi.as<double>(), c->s_rf.as<float>(), c->s_invd.as<float>()};
+  A.q = QRec{c->s_phi.as<double>()};
   A.a = M->cosh_r_minus_1;
   // one warp walks a whole tile, so a tile of 32 queries at the limit bounds
   // the light pass from below (~0.35 ms at 2048): sharded runs, whose light
@@ -918,7 +917,7 @@ hrg_status hrg_context_destroy(hrg_context* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (Buf* b : {&c->phi, &c->rn, &c->rp, &c->keys_out, &c->vals_in, &c->vals_out,
-                 &c->pt, &c->circ, &c->s_phi, &c->s_rf, &c->s_invd, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
+                 &c->pt, &c->circ, &c->s_phi, &c->s_rp, &c->s_rn, &c->pr, &c->stage,
                  &c->stage_off, &c->counters, &c->heavy_v, &c->heavy_c, &c->heavy_of,
                  &c->nchunks, &c->chunk_start, &c->chunk_hits, &c->chunk_entry, &c->chunk_off,
                  &c->slots,

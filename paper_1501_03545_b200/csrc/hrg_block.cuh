@@ -223,7 +223,7 @@ k_block(QueryArgs A, const int64_t* __restrict__ rowptr, int64_t nrows, int32_t*
     __syncwarp();
     if (act) qs[lane] = load_qb<kSampleIds>(A, v);
     const double phi = act ? A.q.phi[v] : 0.0;
-    const float rf = act ? A.q.rf[v] : 3.0e38f;
+    const float rf = act ? __ldg(&A.rec.circ[v].rf) : 3.0e38f;
     const int32_t row = act ? row_of<kSampleIds>(A, v) : 0;
     // write pass: the tile's rows (lengths known from the count pass) go to
     // a shared buffer at exact offsets when they fit -- then every lane sorts

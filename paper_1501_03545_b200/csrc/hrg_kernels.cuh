@@ -285,7 +285,9 @@ __global__ void __launch_bounds__(256) k_keys_from_coords(int64_t n, const doubl
 // (c_x, c_y, rad^2), 32 B, for the query side and for pred(w -> v) inside the
 // rounding margin; the vertex id (4 B, the sort permutation) beside them.
 struct __align__(16) Circ {
-  double cx, cy, rsq, pad;
+  double cx, cy, rsq;
+  float rf;    // a lower bound of the hyperbolic radius 2 atanh(r) (window-table row)
+  float invd;  // an upper bound of 1 / D, D = a (1 - r)(1 + r) + 2 (the pair test's margin)
 };
 
 struct Recs {
@@ -296,8 +298,6 @@ struct Recs {
 
 struct QRec {          // query-side extras, per sorted position
   double* phi;
-  float* rf;           // a lower bound of the hyperbolic radius 2*atanh(r)
-  float* invd;         // an upper bound of 1 / D, D = a (1 - r)(1 + r) + 2 (see walk_test)
 };
 
 // Gather into (band, angle) order and precompute every per-point quantity the
@@ -360,16 +360,13 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
   const double px = __dmul_rn(r, cs), py = __dmul_rn(r, sn);
   const double cx = __dmul_rn(cr, cs), cy = __dmul_rn(cr, sn), rsq = __dmul_rn(rad, rad);
   rec.pt[p] = make_double2(px, py);
+  Circ ci;
+  ci.cx = cx; ci.cy = cy; ci.rsq = rsq;
   {
     // 1 / D rounded up (float) with 2^-18 of slack: D = a b + 2 errs by a few
     // ulps here, the walk's margin only needs an upper bound
     const double D = a * ((1.0 - r) * (1.0 + r)) + 2.0;
-    q.invd[p] = __double2float_ru(1.0 / D) * (1.0f + 0x1p-18f);
-  }
-  {
-    Circ ci;
-    ci.cx = cx; ci.cy = cy; ci.rsq = rsq; ci.pad = 0.0;
-    rec.circ[p] = ci;
+    ci.invd = __double2float_ru(1.0 / D) * (1.0f + 0x1p-18f);
   }
   q.phi[p] = ph;
   // a lower bound of the hyperbolic radius of the stored Poincare point,
@@ -378,7 +375,8 @@ __global__ void __launch_bounds__(256) k_gather(int64_t n, const int32_t* perm,
   // 1 - r exact in double (r <= 1 - 2^-53), then 1e-5 relative and 1e-5
   // absolute taken off (float log and division err by < 1e-6 relative)
   const float lr = __logf(__fdividef((float)(1.0 + r), (float)(1.0 - r)));
-  q.rf[p] = fmaxf(0.0f, lr * (1.0f - 1e-5f) - 1e-5f);
+  ci.rf = fmaxf(0.0f, lr * (1.0f - 1e-5f) - 1e-5f);
+  rec.circ[p] = ci;
   if (s_rp) s_rp[p] = r;
   if (s_rn) s_rn[p] = rn[i];
 }
@@ -1036,7 +1034,10 @@ __device__ __forceinline__ Circ load_circ(const Recs& R, int32_t w) {
   const double2* q = reinterpret_cast<const double2*>(R.circ + w);
   const double2 a = __ldg(q), b = __ldg(q + 1);
   Circ c;
-  c.cx = a.x; c.cy = a.y; c.rsq = b.x; c.pad = 0.0;
+  c.cx = a.x; c.cy = a.y; c.rsq = b.x;
+  const long long bits = __double_as_longlong(b.y);  // (rf, invd) as two floats
+  c.rf = __int_as_float((int)(bits & 0xffffffffll));
+  c.invd = __int_as_float((int)(bits >> 32));
   return c;
 }
 
@@ -1240,7 +1241,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     int32_t c = 0;
     bool ovf = false;
     const double phi = active ? A.q.phi[v] : 0.0;
-    const float rvq = active ? A.q.rf[v] : 3.0e38f;
+    const float rvq = active ? __ldg(&A.rec.circ[v].rf) : 3.0e38f;
     const uint32_t q32 = (uint32_t)(qkey(phi, A.C) >> (kQBits - 32));
     const uint32_t* wrowq = A.wtab_q + (wtab_row(A, rvq) - A.wtab);
     // ---- tile-level union windows (lane = band): the 32 queries are
@@ -1402,7 +1403,7 @@ __global__ void __launch_bounds__(kLightThreads, kMinBlocks) k_light(QueryArgs A
     float invd = 0.0f;
     if (light) {
       f = load_query<kSampleIds>(A, v);
-      invd = A.q.invd[v];
+      invd = __ldg(&A.rec.circ[v].invd);
       QHot h;
       h.cx = f.cx; h.cy = f.cy; h.rsq = f.rsq; h.invd = invd; h.idv = f.idv;
       sm.qh[tid] = h;
@@ -1719,11 +1720,11 @@ __global__ void __launch_bounds__(256, HRG_HEAVY_MINB) k_heavy(QueryArgs A, int6
     const int32_t v = A.heavy_v[e];
     const int64_t local = c - A.chunk_start[e];
     QFull f = load_query<kSampleIds>(A, v);
-    const float invd = A.q.invd[v];
+    const float invd = __ldg(&A.rec.circ[v].invd);
     int32_t sA = 0, eA = 0, sB = 0, eB = 0;
     float ed = 0.0f;  // lane = band: e * D of its innermost point (the walk's margin)
     if (lane < A.L) {
-      const float* wrow = wtab_row(A, A.q.rf[v]);
+      const float* wrow = wtab_row(A, __ldg(&A.rec.circ[v].rf));
       union_window(A, sb[lane], A.q.phi[v], __ldg(wrow + lane), sA, eA, sB, eB);
       const double D = A.a * ((1.0 - sb[lane].pmin) * (1.0 + sb[lane].pmin)) + 2.0;
       ed = __double2float_ru(0x1p-45 * D) * (1.0f + 0x1p-18f);
